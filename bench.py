@@ -1,0 +1,339 @@
+"""Jacobi3D weak-scaling bench on B200 (BASELINE.json configs[2]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...   (one rank per GPU)
+
+Workload: 1536^3 fp64 cells per GPU, global grid 1536 x (1,1,1)/(2,1,1)/
+(2,2,1)/(2,2,2) at N = 1/2/4/8 (x, y, z doubling),
+decomposed by the reference's decompose (cl/jacobi3d.py:62-76). A step is
+one full iteration over all ranks: fused pack+NVLink put+flag, wait+unpack,
+TMA stencil (paper_2102_12416_b200/halo.py). Inputs (two 29 GB fields per
+GPU) are far larger than L2, so no flush is needed between steps.
+
+Printed JSON line (rank 0): value = whole-job GLUP/s (interior cells x
+steps / max-over-ranks device time), roofline of the stencil kernel vs the
+measured HBM copy peak, cpu_baseline (the C oracle on the host cores, a
+bounded slab sample), e2e through the public API with host buffers
+(per-step H2D of the Dirichlet hot-wall plane from pinned memory, per-step
+D2H of the residual), clocks sampled during the timed region.
+
+--impl reference: the reference's own CPU algorithm (its C restatement in
+oracle/, bit-identical to the numpy reference) on all host cores, same
+metric/config, each step a bounded slab sample of the per-GPU block.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Jacobi3D ms/iter & GLUP/s at 1/2/4/8 B200; p2p halo GB/s & 8B latency"
+UNIT = "GLUP/s"
+BLOCK = 1536
+ALG_BYTES_PER_CELL = 16  # 8 B read + 8 B written per interior cell
+NVLINK_GBS = 900.0
+
+
+def global_dims(n: int, block: int):
+    doubling = {1: (1, 1, 1), 2: (2, 1, 1), 4: (2, 2, 1), 8: (2, 2, 2)}
+    if n not in doubling:
+        raise SystemExit(f"--gpus must be 1, 2, 4 or 8 (got {n})")
+    return tuple(block * f for f in doubling[n])
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per stencil launch from the committed ncu --set full summary."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "stencil_ncu_summary.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([c.strip() for c in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.rows)}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_sample(block: int, seconds: float):
+    """The C oracle (all host cores) on a bounded slab of the per-GPU block:
+    64 x-planes of the full block cross-section, swept until ~seconds pass."""
+    import numpy as np
+
+    from oracle import jacobi_c
+
+    planes = 64
+    cur = np.zeros((planes + 2, block + 2, block + 2))
+    cur[0] = 1.0
+    nxt = cur.copy()
+    nth = cpu_threads()
+    jacobi_c.stencil(cur, nxt, nth)  # warm
+    sweeps, t0 = 0, time.perf_counter()
+    while True:
+        jacobi_c.stencil(cur, nxt, nth)
+        cur, nxt = nxt, cur
+        sweeps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    cells = planes * block * block
+    return {"value": cells * sweeps / el / 1e9, "unit": UNIT, "cores": nth, "kind": "port",
+            "sample": f"C oracle (oracle/jacobi_c.c, {nth} pthreads) on a {planes}x{block}x{block} "
+                      f"slab of the {block}^3 block, {sweeps} sweeps in {el:.1f} s"}
+
+
+# ------------------------------------------------------------- reference arm
+
+def run_reference(args, rank: int) -> int:
+    if rank != 0:
+        return 0
+    n = args.gpus
+    dims = global_dims(n, args.block)
+    per_step = max(1.0, args.ref_seconds / max(1, args.steps))
+    for _ in range(args.warmup):
+        cpu_sample(args.block, min(per_step, 2.0))
+    vals = [cpu_sample(args.block, per_step) for _ in range(args.steps)]
+    v = statistics.median(x["value"] for x in vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": n,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": args.block ** 3 * n / (v * 1e9) * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
+            "config": {"workload": "Jacobi3D 1536^3 per GPU fp64 weak scaling",
+                       "global_dims": list(dims), "block": [args.block] * 3},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
+                             "sample": vals[0]["sample"]},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ our arm
+
+def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--block", type=int, default=BLOCK)
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-seconds", type=float, default=60.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}; launch N>1 with torchrun")
+    if args.warmup < 3:
+        raise SystemExit("--warmup must be >= 3")
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2102_12416_b200 import _lib
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dims = global_dims(world, args.block)
+    eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: local,
+                     dist=dist if world > 1 else None)
+    b = eng.blocks[rank]
+    s = eng.stream_of(b)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-timed steps (inputs resident in HBM)
+    for _ in range(args.warmup):
+        eng.step()
+    barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    xev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        start.record(s)
+        for k in range(args.steps):
+            xev[k][0].record(s)
+            if b.nbr_dirs:
+                eng._put(b, eng.it)
+                eng._wait(b, eng.it)
+            xev[k][1].record(s)
+            ev[k][0].record(s)
+            eng._relax(b, None)
+            ev[k][1].record(s)
+            eng.it += 1
+        stop.record(s)
+        barrier()
+    eng.check_errors()
+    t_ms = max_over_ranks(start.elapsed_time(stop))
+    sten_ms = statistics.mean(a.elapsed_time(z) for a, z in ev)
+    xch_ms = max_over_ranks(statistics.mean(a.elapsed_time(z) for a, z in xev))
+    launches = args.steps * (1 + (2 if b.nbr_dirs else 0)) * world
+    cells = b.cells
+    total_cells = cells * world
+    value = total_cells * args.steps / (t_ms * 1e-3) / 1e9
+    peak, peak_kind = hbm_peak()
+    achieved = ALG_BYTES_PER_CELL * cells / (sten_ms * 1e-3) / 1e9
+    face_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs)
+
+    # ---- end to end through the public API with host buffers
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(eng, b, args, world, barrier, max_over_ranks, total_cells)
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_sample(args.block, args.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
+            "config": {"workload": "Jacobi3D 1536^3 per GPU fp64 weak scaling",
+                       "global_dims": list(dims), "grid": list(eng.grid),
+                       "block": [b.bx, b.by, b.bz], "parallelism": f"3d-blocks x{world}",
+                       "l2": "inputs > L2 (2 x 29 GB fields per GPU), no flush needed"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "kernel": "stencil_tma_kernel", "peak_kind": peak_kind,
+                         "kernel_ms": sten_ms,
+                         "alg_bytes_per_launch": ALG_BYTES_PER_CELL * cells},
+            "halo": ({"bytes_out_per_rank": face_bytes, "exchange_ms": xch_ms,
+                      "exchange_gbs": face_bytes / (xch_ms * 1e-3) / 1e9,
+                      "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS,
+                      "non_overlapped_frac": xch_ms / (t_ms / args.steps)} if world > 1 else None),
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(eng, b, args, world, barrier, max_over_ranks, total_cells):
+    """Public-API steps with host buffers: each step uploads the Dirichlet
+    hot-wall plane (ranks on the global x=0 face) from pinned memory and
+    reads the step's residual back to pinned host memory."""
+    import torch
+
+    hot = b.coords[0] == 0
+    plane = (b.by + 2) * (b.bz + 2)
+    host_wall = torch.ones(plane, dtype=torch.float64, pin_memory=True)
+    res_host = torch.zeros(args.steps + args.warmup, dtype=torch.int64, pin_memory=True)
+    for k in range(args.warmup):
+        eng.step_e2e(host_wall if hot else None, res_host[k:k + 1])
+    barrier()
+    t0 = time.perf_counter()
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
+    s = eng.stream_of(b)
+    start.record(s)
+    for k in range(args.warmup, args.warmup + args.steps):
+        eng.step_e2e(host_wall if hot else None, res_host[k:k + 1])
+    eng.drain_e2e()
+    stop.record(s)
+    barrier()
+    wall_ms = (time.perf_counter() - t0) * 1e3
+    t_ms = max_over_ranks(max(start.elapsed_time(stop), wall_ms))
+    eng.check_errors()
+    h2d = torch.tensor([plane * 8 if hot else 0], dtype=torch.int64)
+    h2d_total = int(h2d.item()) * (world // eng.grid[0])  # ranks on the x=0 face
+    res = res_host.numpy().view("float64")
+    return {"value": total_cells * args.steps / (t_ms * 1e-3) / 1e9, "unit": UNIT,
+            "h2d_bytes_per_step": h2d_total, "d2h_bytes_per_step": 8 * world,
+            "ms_per_step": t_ms / args.steps, "last_residual": float(res[-1]),
+            "api": "paper_2102_12416_b200.halo.HaloJacobi.step_e2e"}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

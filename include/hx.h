@@ -1,0 +1,163 @@
+/* hx.h — C ABI of the B200 halo-exchange library (libhx.so).
+ *
+ * The reference (charmlet, /root/reference/pkg/src/charmlet = cl/) has no
+ * native plugin layer: its hot path is numpy over a simulated device space.
+ * This ABI sits UNDER the reference's unchanged Python API (DeviceSpace,
+ * Worker.tag_send/tag_recv, Channel, devmsg, _BlockCore, run_jacobi) and is
+ * bound with ctypes. Each entry point names the
+ * reference interface it replaces.
+ *
+ * Conventions
+ *  - Every function returns int: 0 = success, >0 = cudaError_t, <0 = HX_E_*.
+ *  - Pointers are device pointers on the CURRENT device (hx_set_device),
+ *    except where a peer-mapped pointer is explicitly allowed.
+ *  - stream: a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Fields are padded fp64 blocks in C order (bx+2, by+2, bz+2): z is
+ *    contiguous, x slowest (cl/jacobi3d.py:131-134). Interior indices run
+ *    1..bx, 1..by, 1..bz; ghosts are planes 0 and n+1.
+ *  - Direction codes d: 0=-x 1=+x 2=-y 3=+y 4=-z 5=+z (cl/jacobi3d.py:35).
+ *  - The library never frees memory it did not allocate.
+ */
+#ifndef HX_H
+#define HX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HX_ABI_VERSION 1
+
+#define HX_E_INVALID   (-1) /* bad argument (shape, direction, null pointer) */
+#define HX_E_TIMEOUT   (-2) /* a device-side flag wait exceeded its deadline */
+#define HX_E_NODRIVER  (-3) /* a driver entry point could not be resolved    */
+#define HX_E_TMA       (-4) /* cuTensorMapEncodeTiled rejected the layout     */
+
+/* ------------------------------------------------------------ runtime ---- */
+int hx_abi_version(void);
+const char *hx_error_string(int code);
+int hx_device_count(int *n);
+int hx_set_device(int dev);
+int hx_get_device(int *dev);
+int hx_sm_count(int dev, int *n);
+int hx_device_synchronize(void);
+int hx_stream_create(void **stream);                 /* non-blocking stream on current dev */
+int hx_stream_destroy(void *stream);
+int hx_stream_synchronize(void *stream);
+int hx_event_create(void **ev, int timing);          /* timing=0: cudaEventDisableTiming */
+int hx_event_destroy(void *ev);
+int hx_event_record(void *ev, void *stream);
+int hx_event_query(void *ev);                        /* 0 done, 1 pending, else error */
+int hx_event_synchronize(void *ev);
+int hx_event_elapsed_ms(void *start, void *stop, float *ms);
+int hx_stream_wait_event(void *stream, void *ev);
+/* Device memory owned by the caller of hx_malloc (IPC arenas only; fields and
+ * staging are torch allocations). */
+int hx_malloc(void **ptr, size_t bytes);
+int hx_free(void *ptr);
+int hx_malloc_host(void **ptr, size_t bytes);        /* pinned host memory */
+int hx_free_host(void *ptr);
+
+/* ---------------------------------------------------- peer access / IPC --
+ * Replaces the reference's in-process byte copies between workers
+ * (cl/devicesim.py:72-86 read_wire/write_wire) with NVLink P2P mappings. */
+int hx_can_access_peer(int dev, int peer, int *ok);
+int hx_enable_peer(int dev, int peer);               /* idempotent */
+/* handle_out: 64-byte cudaIpcMemHandle_t of the allocation holding ptr;
+ * offset_out: ptr - allocation base. */
+int hx_ipc_get(void *ptr, void *handle_out, size_t *offset_out);
+int hx_ipc_open(const void *handle, void **base_out); /* cached per handle */
+int hx_ipc_close(void *base);
+
+/* --------------------------------------------------------------- copies --
+ * cl/devicesim.py:197-224 (host_to_device / device_to_host /
+ * device_to_device) and the transport's device payload moves
+ * (cl/transport.py:284-289, 430-432, 459-463). */
+int hx_memcpy(void *dst, const void *src, size_t bytes, void *stream);          /* cudaMemcpyDefault */
+int hx_memcpy_peer(void *dst, int dst_dev, const void *src, int src_dev, size_t bytes, void *stream);
+int hx_copy_sm(void *dst, const void *src, size_t bytes, void *stream);         /* SM-issued (peer ok) */
+int hx_fill_f64(double *dst, size_t n, double value, void *stream);
+
+/* ------------------------------------------------------------- stencil ---
+ * _BlockCore.update, cl/jacobi3d.py:165-173:
+ *   nxt[i,j,k] = (((((cur[i-1,j,k] + cur[i+1,j,k]) + cur[i,j-1,k])
+ *                 + cur[i,j+1,k]) + cur[i,j,k-1]) + cur[i,j,k+1]) / 6.0
+ * for every interior cell; ghosts of nxt untouched. Bit-exact with the
+ * reference (IEEE adds in this order, correctly rounded division).
+ * res (nullable): device uint64 holding the bit pattern of a non-negative
+ * double; the kernel atomically maxes max|nxt - cur| into it
+ * (cl/jacobi3d.py:197-198). The caller zeroes it. */
+int hx_stencil(const double *cur, double *nxt, int bx, int by, int bz,
+               unsigned long long *res, void *stream);
+/* Sub-box of the interior, 1-based inclusive-exclusive [i0,i1)x[j0,j1)x[k0,k1);
+ * used for the interior/boundary-shell overlap split. */
+int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz,
+                   int i0, int i1, int j0, int j1, int k0, int k1,
+                   unsigned long long *res, void *stream);
+/* Force a kernel variant (testing / profiling): 0 auto, 1 TMA pipeline,
+ * 2 generic. Returns the previous setting. */
+int hx_stencil_set_variant(int variant);
+int hx_stencil_last_variant(void);
+/* Tuning knob for the TMA pipeline: x planes per CTA work item (0 = auto). */
+int hx_stencil_set_chunk(int planes);
+
+/* Hot-wall / Dirichlet initialisation of one padded block
+ * (cl/jacobi3d.py:135-138, 186-188): every cell = background, interior =
+ * fill, and if hot_wall the whole x=0 ghost plane = hot. */
+int hx_init_block(double *field, int bx, int by, int bz, int hot_wall,
+                  double hot, double background, double fill, void *stream);
+
+/* -------------------------------------------------------- pack / unpack --
+ * _BlockCore.pack (cl/jacobi3d.py:157-158): dst = C-order copy of interior
+ * plane 1 (d even) or n (d odd) of axis d/2 over the other two interior
+ * axes (face_shape, cl/jacobi3d.py:141-144). dst may be a peer-mapped
+ * pointer (fused pack + NVLink put). */
+int hx_pack(const double *field, int bx, int by, int bz, int d, double *dst, void *stream);
+/* _BlockCore.unpack_all for one direction (cl/jacobi3d.py:160-163): write
+ * a face into ghost plane 0 (d even) or n+1 (d odd). src may be peer-mapped. */
+int hx_unpack(double *field, int bx, int by, int bz, int d, const double *src, void *stream);
+
+/* Fused multi-face pack + put + signal (Channel.send of every halo face,
+ * cl/jacobi3d.py:250-253, without per-message metadata): for each d in
+ * dir_mask, pack face d into dst[d] (typically the neighbour's receive slot,
+ * peer-mapped) and, once every CTA of that face has stored, publish
+ * *flag[d] = value with system-scope release. counters: 6 device uint32,
+ * zero-initialised once; the kernel returns them to zero. flag[d] may be
+ * NULL (no signal). */
+int hx_pack_put(const double *field, int bx, int by, int bz, int dir_mask,
+                double *const dst[6], unsigned long long *const flag[6],
+                unsigned long long value, unsigned int *counters, void *stream);
+/* Fused wait + multi-face unpack (Channel.recv completions + unpack_all,
+ * cl/jacobi3d.py:254-257, 277): for each d in dir_mask wait until
+ * *flag[d] >= value (system-scope acquire; bounded by timeout_ns, then
+ * *err = HX_E_TIMEOUT and the face is skipped), then unpack src[d]. */
+int hx_wait_unpack(double *field, int bx, int by, int bz, int dir_mask,
+                   const double *const src[6], unsigned long long *const flag[6],
+                   unsigned long long value, unsigned long long timeout_ns, int *err,
+                   void *stream);
+
+/* ---------------------------------------------------------------- flags --
+ * Persistent-channel completion words (the Channel API's per-direction
+ * counter, cl/channels.py:75-99, carried as a 64-bit flag value). */
+int hx_signal(unsigned long long *flag, unsigned long long value, void *stream);
+int hx_wait_flag(unsigned long long *flag, unsigned long long value,
+                 unsigned long long timeout_ns, int *err, void *stream);
+int hx_read_u64(const unsigned long long *dev_ptr, unsigned long long *host_out); /* sync read */
+
+/* ------------------------------------------------- device-level ping-pong --
+ * OSU latency inner loop (cl/bench.py:170-194) with kernel-issued NVLink
+ * stores: iters round trips of `bytes` between two GPUs. Leader (role 0)
+ * writes payload into peer_buf then flag; follower (role 1) echoes.
+ * Both kernels must run concurrently on DIFFERENT GPUs. elapsed_ns (device
+ * uint64, leader only) receives %globaltimer delta over the timed iters. */
+int hx_pingpong(int role, const void *src, void *peer_dst, size_t bytes,
+                unsigned long long *my_flag, unsigned long long *peer_flag,
+                int iters, int warmup, unsigned long long timeout_ns,
+                unsigned long long *elapsed_ns, int *err, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HX_H */

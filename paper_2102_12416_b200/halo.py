@@ -1,0 +1,378 @@
+"""Persistent-channel Jacobi3D engine: one block per GPU, NVLink peer puts.
+
+This is the B200 form of the paper's Channel API applied to the Jacobi3D
+halo exchange (paper §3.2.2 + §4.3; reference loop cl/jacobi3d.py:246-279,
+channels cl/channels.py:75-99). Each block owns an IPC-exportable receive
+arena in HBM:
+
+    [flags: 6 x u64][counters: 6 x u32][err: i32][pad][slot[parity][dir] ...]
+
+created once and mapped by its neighbours (CUDA IPC handle cache across
+processes, plain P2P pointers inside one process). Per iteration, on one
+stream per GPU and with no host involvement:
+
+  1. hx_pack_put: pack every neighbour-facing interior plane straight into
+     the neighbour's slot[it & 1][d ^ 1] over NVLink (fused pack + put) and,
+     once all CTAs of that face have stored, release-store flag = it + 1 in
+     the neighbour's arena — the channel counter is the flag value, so no
+     tag or metadata ever crosses (paper Fig. 6-7);
+  2. hx_wait_unpack: acquire own flags >= it + 1 and unpack the slots into
+     the ghost planes;
+  3. hx_stencil (TMA pipeline) cur -> nxt, optional fused residual.
+
+Two parity slots suffice: a neighbour can run at most one iteration ahead
+(cl/jacobi3d.py:146) because its put for it + 2 needs our flag for it + 1,
+which we publish only after unpacking iteration it.
+
+Blocks hosted by the same process (the single-GPU emulation used by the
+tests) are driven on ONE stream in phase order — all puts, then all waits,
+then all stencils — so a wait never precedes the put it depends on and no
+two waiting kernels ever need to be co-resident on a GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from .jacobi3d import _block_coords, decompose, decompose_b200, neighbor_table
+
+NDIRS = 6
+_ALIGN = 256
+_HDR = 256  # flags (48 B) + counters (24 B) + err (4 B), padded
+
+
+def _round(n: int) -> int:
+    return (n + _ALIGN - 1) // _ALIGN * _ALIGN
+
+
+class HaloBlock:
+    """One block: two padded fields + its receive arena on one GPU."""
+
+    def __init__(self, dims, grid, rank: int, device: int, allocate: bool = True):
+        self.rank = rank
+        self.grid = grid
+        self.device = device
+        self.bx, self.by, self.bz = dims[0] // grid[0], dims[1] // grid[1], dims[2] // grid[2]
+        self.coords = _block_coords(rank, grid)
+        self.neighbors = neighbor_table(grid, rank)
+        self.nbr_dirs = [d for d in range(NDIRS) if self.neighbors[d] is not None]
+        self.dir_mask = sum(1 << d for d in self.nbr_dirs)
+        ext = (self.bx, self.by, self.bz)
+        self.face_elems = [int(np.prod([ext[a] for a in range(3) if a != d // 2])) for d in range(NDIRS)]
+        self.slot_off = {}
+        off = _HDR
+        for p in (0, 1):
+            for d in range(NDIRS):
+                self.slot_off[(p, d)] = off
+                off += _round(self.face_elems[d] * 8)
+        self.arena_bytes = off
+        self.cur = 0
+        self.fields, self.arena = [], None
+        if allocate:
+            dev = torch.device("cuda", device)
+            shape = (self.bx + 2, self.by + 2, self.bz + 2)
+            self.fields = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
+            self.arena = torch.zeros(self.arena_bytes, dtype=torch.uint8, device=dev)
+        # filled by HaloJacobi.connect(): (neighbour arena base, its side)
+        self.put_dst = [None] * NDIRS
+        self.put_flag = [None] * NDIRS
+
+    @property
+    def base(self) -> int:
+        return self.arena.data_ptr()
+
+    def link(self, d: int, peer_base: int) -> None:
+        """Point face d's put at the neighbour's arena: I send face d, the
+        neighbour receives it on its side d ^ 1 (slot and flag)."""
+        self.put_dst[d] = (peer_base, d ^ 1)
+        self.put_flag[d] = self.flag_ptr(d ^ 1, peer_base)
+
+    def put_slot(self, d: int, parity: int) -> int:
+        base, side = self.put_dst[d]
+        return base + self.slot_off[(parity, side)]
+
+    def flag_ptr(self, d: int, base: int | None = None) -> int:
+        return (self.base if base is None else base) + 8 * d
+
+    @property
+    def counters_ptr(self) -> int:
+        return self.base + 48
+
+    @property
+    def err_ptr(self) -> int:
+        return self.base + 72
+
+    def slot_ptr(self, parity: int, d: int, base: int | None = None) -> int:
+        return (self.base if base is None else base) + self.slot_off[(parity, d)]
+
+    def field_ptr(self, which: int | None = None) -> int:
+        return self.fields[self.cur if which is None else which].data_ptr()
+
+    @property
+    def cells(self) -> int:
+        return self.bx * self.by * self.bz
+
+
+def exchange_table(dist, mine):
+    """All-gather each process's (rank, ipc handle, offset, device) arena
+    records — the one-time persistent-channel set-up. Without a process
+    group every block is local and the table is just ``mine``."""
+    if dist is None:
+        return {r: (h, o, dv) for (r, h, o, dv) in mine}
+    gathered = [None] * dist.get_world_size()
+    dist.all_gather_object(gathered, mine)
+    return {r: (h, o, dv) for part in gathered for (r, h, o, dv) in part}
+
+
+class HaloJacobi:
+    """Jacobi3D over persistent NVLink channels.
+
+    dims: global grid; pes: total blocks; local_ranks: blocks hosted by this
+    process; device_of(rank) -> CUDA ordinal; group: torch.distributed
+    process group (None when every block is local). policy "reference"
+    uses cl/jacobi3d.py's decompose (bit-for-bit the reference's block
+    layout); "b200" prefers not to split z on ties.
+    """
+
+    def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
+                 policy: str = "reference", timeout_s: float = 30.0):
+        self.dims = tuple(dims)
+        self.pes = pes
+        self.grid = (decompose if policy == "reference" else decompose_b200)(self.dims, pes)
+        self.local_ranks = list(range(pes)) if local_ranks is None else list(local_ranks)
+        ndev = max(1, torch.cuda.device_count())
+        self.device_of = device_of or (lambda r: r % ndev)
+        self.dist = dist
+        self.timeout_ns = int(timeout_s * 1e9)
+        self.blocks = {r: HaloBlock(self.dims, self.grid, r, self.device_of(r)) for r in self.local_ranks}
+        self.streams = {}
+        for b in self.blocks.values():
+            if b.device not in self.streams:
+                self.streams[b.device] = torch.cuda.Stream(device=b.device)
+        self.it = 0
+        self._ipc_bases = []
+        self._res = {}
+        self.reset()
+        self.connect()
+
+    # ------------------------------------------------------------ set-up --
+
+    def stream_of(self, b: HaloBlock) -> torch.cuda.Stream:
+        return self.streams[b.device]
+
+    def reset(self) -> None:
+        """Dirichlet initial state (cl/jacobi3d.py:131-138) and zeroed flags."""
+        for b in self.blocks.values():
+            s = self.stream_of(b).cuda_stream
+            _lib.call("hx_set_device", b.device)
+            for f in b.fields:
+                _lib.call("hx_init_block", f.data_ptr(), b.bx, b.by, b.bz,
+                          int(b.coords[0] == 0), 1.0, 0.0, 0.0, s)
+            with torch.cuda.stream(self.stream_of(b)):
+                b.arena[:_HDR].zero_()
+            b.cur = 0
+        self.it = 0
+        self.synchronize()
+
+    def connect(self) -> None:
+        """Exchange receive-arena addresses once (the persistent channel set-up)."""
+        mine = []
+        for r, b in self.blocks.items():
+            handle = (ctypes.c_char * 64)()
+            off = ctypes.c_size_t(0)
+            if self.dist is not None:
+                _lib.call("hx_set_device", b.device)
+                _lib.call("hx_ipc_get", b.base, handle, ctypes.byref(off))
+            mine.append((r, bytes(handle), off.value, b.device))
+        table = exchange_table(self.dist, mine)
+        bases = {}
+        for r, b in self.blocks.items():
+            for d in b.nbr_dirs:
+                n = b.neighbors[d]
+                if n in self.blocks:
+                    bases[n] = self.blocks[n].base
+                    if self.blocks[n].device != b.device:
+                        _lib.call("hx_enable_peer", b.device, self.blocks[n].device)
+                elif n not in bases:
+                    h, o, _ = table[n]
+                    base = ctypes.c_void_p()
+                    _lib.call("hx_set_device", b.device)
+                    _lib.call("hx_ipc_open", h, ctypes.byref(base))
+                    self._ipc_bases.append(base.value)
+                    bases[n] = base.value + o
+                b.link(d, bases[n])
+
+    # ------------------------------------------------------------- steps --
+
+    def _put(self, b: HaloBlock, it: int) -> None:
+        p = it & 1
+        dst = [None] * NDIRS
+        flg = [None] * NDIRS
+        for d in b.nbr_dirs:
+            dst[d] = b.put_slot(d, p)
+            flg[d] = b.put_flag[d]
+        _lib.call("hx_pack_put", b.field_ptr(), b.bx, b.by, b.bz, b.dir_mask, _lib.ptr_array(dst),
+                  _lib.ptr_array(flg), it + 1, b.counters_ptr, self.stream_of(b).cuda_stream)
+
+    def _wait(self, b: HaloBlock, it: int) -> None:
+        p = it & 1
+        src = [b.slot_ptr(p, d) if d in b.nbr_dirs else None for d in range(NDIRS)]
+        flg = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
+        _lib.call("hx_wait_unpack", b.field_ptr(), b.bx, b.by, b.bz, b.dir_mask,
+                  _lib.ptr_array(src), _lib.ptr_array(flg), it + 1, self.timeout_ns, b.err_ptr,
+                  self.stream_of(b).cuda_stream)
+
+    def _relax(self, b: HaloBlock, res_ptr) -> None:
+        _lib.call("hx_stencil", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz, res_ptr,
+                  self.stream_of(b).cuda_stream)
+        b.cur ^= 1
+
+    def step(self, residual: bool = False) -> None:
+        """One iteration on every local block (enqueue only, no host sync)."""
+        it = self.it
+        blocks = list(self.blocks.values())
+        for b in blocks:
+            if b.nbr_dirs:
+                _lib.call("hx_set_device", b.device)
+                self._put(b, it)
+        for b in blocks:
+            if b.nbr_dirs:
+                _lib.call("hx_set_device", b.device)
+                self._wait(b, it)
+        for b in blocks:
+            _lib.call("hx_set_device", b.device)
+            res_ptr = None
+            if residual:
+                buf = self._res.setdefault(b.rank, [])
+                if len(buf) <= it:
+                    t = torch.zeros(1, dtype=torch.int64, device=f"cuda:{b.device}")
+                    buf.append(t)
+                res_ptr = buf[it].data_ptr()
+            self._relax(b, res_ptr)
+        self.it += 1
+
+    def run(self, iters: int, residual: bool = False) -> None:
+        for _ in range(iters):
+            self.step(residual)
+
+    # ------------------------------------------------- host-buffer steps --
+
+    def step_e2e(self, host_wall=None, res_out=None) -> None:
+        """One iteration fed from / reported to HOST memory (public API).
+
+        host_wall: pinned fp64 host tensor of (by+2)*(bz+2) values, the
+        Dirichlet x=0 ghost plane (cl/jacobi3d.py:137-138), uploaded into
+        every local block on the global x=0 face; res_out: pinned int64 host
+        tensor with one slot per local block receiving the bit pattern of
+        that block's max|nxt-cur| (cl/jacobi3d.py:197).
+        The upload for step it only has to wait for the sweep of it-2 (the
+        last reader of that buffer's ghost plane), so it overlaps the sweep
+        of it-1; the residual read-back trails the sweep on a copy stream.
+        """
+        it = self.it
+        st = self._e2e_state()
+        blocks = list(self.blocks.values())
+        for b in blocks:
+            if host_wall is not None and b.coords[0] == 0:
+                if host_wall.numel() != (b.by + 2) * (b.bz + 2) or host_wall.dtype != torch.float64:
+                    raise ValueError(f"host_wall must hold {(b.by + 2) * (b.bz + 2)} fp64 values")
+                if not host_wall.is_pinned():
+                    raise ValueError("host_wall must be pinned host memory")
+                cs = st["copy"][b.device]
+                prev = st["sweep_done"].get((b.rank, it - 2))
+                if prev is not None:
+                    cs.wait_event(prev)
+                _lib.call("hx_set_device", b.device)
+                _lib.call("hx_memcpy", b.field_ptr(), host_wall.data_ptr(),
+                          host_wall.numel() * 8, cs.cuda_stream)
+                up = torch.cuda.Event()
+                up.record(cs)
+                st["uploaded"][b.rank] = up
+        for b in blocks:
+            if b.nbr_dirs:
+                _lib.call("hx_set_device", b.device)
+                self._put(b, it)
+        for b in blocks:
+            if b.nbr_dirs:
+                _lib.call("hx_set_device", b.device)
+                self._wait(b, it)
+        for b in blocks:
+            _lib.call("hx_set_device", b.device)
+            s = self.stream_of(b)
+            up = st["uploaded"].pop(b.rank, None)
+            if up is not None:
+                s.wait_event(up)
+            ring = st["ring"][b.rank]
+            slot = it % ring.numel()
+            if slot == 0:
+                with torch.cuda.stream(s):
+                    ring.zero_()
+            self._relax(b, ring.data_ptr() + 8 * slot)
+            done = torch.cuda.Event()
+            done.record(s)
+            st["sweep_done"][(b.rank, it)] = done
+            st["sweep_done"].pop((b.rank, it - 3), None)
+            if res_out is not None:
+                cs = st["copy"][b.device]
+                cs.wait_event(done)
+                _lib.call("hx_memcpy", res_out.data_ptr() + 8 * blocks.index(b),
+                          ring.data_ptr() + 8 * slot, 8, cs.cuda_stream)
+        self.it += 1
+
+    def drain_e2e(self) -> None:
+        st = self._e2e_state()
+        for cs in st["copy"].values():
+            cs.synchronize()
+        self.synchronize()
+
+    def _e2e_state(self):
+        st = getattr(self, "_e2e", None)
+        if st is None:
+            st = self._e2e = {
+                "copy": {d: torch.cuda.Stream(device=d) for d in self.streams},
+                "ring": {r: torch.zeros(4096, dtype=torch.int64, device=f"cuda:{b.device}")
+                         for r, b in self.blocks.items()},
+                "sweep_done": {}, "uploaded": {},
+            }
+        return st
+
+    def synchronize(self) -> None:
+        for s in self.streams.values():
+            s.synchronize()
+
+    def check_errors(self) -> None:
+        self.synchronize()
+        for b in self.blocks.values():
+            err = int(b.arena[72:76].view(torch.int32).item())
+            if err != 0:
+                raise RuntimeError(f"block {b.rank}: device error {err} ({_lib.error_string(err)})")
+
+    # ------------------------------------------------------------ results --
+
+    def interior_host(self, rank: int) -> np.ndarray:
+        b = self.blocks[rank]
+        self.stream_of(b).synchronize()
+        return b.fields[b.cur][1:-1, 1:-1, 1:-1].cpu().numpy()
+
+    def residuals(self, rank: int) -> list:
+        self.synchronize()
+        return [float(t.cpu().numpy().view(np.float64)[0]) for t in self._res.get(rank, [])]
+
+    def assemble(self) -> np.ndarray:
+        """Global interior (all blocks must be local)."""
+        out = np.empty(self.dims)
+        bx, by, bz = (self.dims[a] // self.grid[a] for a in range(3))
+        for r in range(self.pes):
+            ix, iy, iz = _block_coords(r, self.grid)
+            out[ix * bx:(ix + 1) * bx, iy * by:(iy + 1) * by, iz * bz:(iz + 1) * bz] = self.interior_host(r)
+        return out
+
+    def close(self) -> None:
+        self.synchronize()
+        for base in self._ipc_bases:
+            _lib.raw("hx_ipc_close")(base)
+        self._ipc_bases = []

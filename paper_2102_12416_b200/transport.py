@@ -1,0 +1,488 @@
+"""Tagged point-to-point transport with a B200 device data plane.
+
+Mirror of cl/transport.py:1-636 (loopback backend): non-blocking tagged
+sends and receives with masked matching — a receive (tag, mask) matches a
+frame when ``frame.tag & mask == tag & mask``; arrivals match the earliest
+posted receive, posts match the earliest unexpected frame, FIFO per
+endpoint pair; eager (<= eager_threshold) vs rendezvous semantics.
+
+What is B200-native (the only place device bytes move):
+  * eager device payloads are snapshotted at send time into a device bounce
+    buffer by a stream-ordered D2D copy (replaces read_wire at
+    cl/transport.py:284-289), so the send completes immediately and the
+    source is reusable, exactly as in the reference;
+  * a matched rendezvous moves the payload with ONE direct device-to-device
+    copy — local HBM or NVLink P2P — from the sender's region into the
+    receiver's sink (replaces the PULL/PAYLOAD byte copies at
+    cl/transport.py:449-465 and the write_wire at 430-432). It is enqueued
+    on the sink owner's stream behind an event recorded on the sender's
+    stream at send time, so no host staging and no extra copy;
+  * host sinks / host payloads use pinned staging + cudaMemcpyAsync;
+  * completions fire from progress() once the CUDA event recorded after the
+    copy has completed (cl/transport.py:342-365), and ``idle`` reports
+    in-flight GPU copies so the runtime never quiesces early
+    (cl/transport.py:372-381, cl/runtime.py:530-542).
+The TCP backend (cl/transport.py:469-586) is out of scope: one box, NVLink.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from collections import Counter, deque
+
+import numpy as np
+import torch
+
+from . import _lib
+from .completion import OK, TRANSPORT_ERROR, TRUNCATED, Completion, deliver
+from .config import RuntimeConfig
+from .device import DeviceBuffer, DeviceRegion, DeviceSpace, as_region
+from .tags import EAGER, FULL_MASK, TagLayout
+from .timebase import WallClock
+
+
+class TransportError(RuntimeError):
+    pass
+
+
+class StartupError(TransportError):
+    pass
+
+
+FRAME_EAGER = 0
+FRAME_RTS = 1
+_NAMES = {FRAME_EAGER: "eager", FRAME_RTS: "rts"}
+
+
+class Frame:
+    """One tagged message in flight. ``source`` is bytes (host) or a
+    DeviceRegion (a bounce snapshot for eager, the sender's region for
+    rendezvous); ``ready`` is the CUDA event after which it may be read."""
+
+    __slots__ = ("kind", "tag", "length", "source", "ready", "src", "send_completion",
+                 "keepalive", "seq")
+
+    def __init__(self, kind, tag, length, source, ready, src, send_completion=None, keepalive=None):
+        self.kind = kind
+        self.tag = tag
+        self.length = length
+        self.source = source
+        self.ready = ready
+        self.src = src
+        self.send_completion = send_completion
+        self.keepalive = keepalive
+        self.seq = 0
+
+    @property
+    def payload(self):
+        return self.source if isinstance(self.source, bytes) else None
+
+    def __repr__(self):
+        return f"Frame({_NAMES[self.kind]}, tag=0x{self.tag:016x}, len={self.length}, src={self.src})"
+
+
+class ReceiveRequest:
+    __slots__ = ("tag", "mask", "capacity", "sink", "completion", "seq", "wildcard", "done")
+
+    def __init__(self, tag, mask, capacity, sink, completion, seq, wildcard=False):
+        self.tag = tag
+        self.mask = mask
+        self.capacity = capacity
+        self.sink = sink
+        self.completion = completion
+        self.seq = seq
+        self.wildcard = wildcard
+        self.done = False
+
+    def matches(self, frame_tag: int) -> bool:
+        return (frame_tag & self.mask) == (self.tag & self.mask)
+
+
+class Endpoint:
+    __slots__ = ("worker", "peer", "failed")
+
+    def __init__(self, worker, peer):
+        self.worker = worker
+        self.peer = peer
+        self.failed = False
+
+
+class _Inflight:
+    """A GPU copy whose completion event gates one or more callbacks."""
+
+    __slots__ = ("event", "fn")
+
+    def __init__(self, event, fn):
+        self.event = event
+        self.fn = fn
+
+
+def _is_device(x) -> bool:
+    return isinstance(x, (DeviceBuffer, DeviceRegion))
+
+
+class Worker:
+    """Matching engine + device data plane for one PE (cl/transport.py:169-598)."""
+
+    def __init__(self, group: "TransportGroup", worker_id: int):
+        self.group = group
+        self.id = worker_id
+        self.cfg = group.cfg
+        self.layout = group.layout
+        self.clock = group.clocks[worker_id]
+        self.posted: list[ReceiveRequest] = []
+        self.unexpected: list[Frame] = []
+        self.inbound: deque = deque()
+        self.endpoints: dict[int, Endpoint] = {}
+        self.stats: Counter = Counter()
+        self.eager_handler = None
+        self.eager_inbox: deque = deque()
+        self._fired: deque = deque()
+        self._inflight: list[_Inflight] = []
+        self._post_seq = 0
+        self._arrival_seq = 0
+        self.hold = None
+        self._held: list = []
+
+    # ------------------------------------------------------------- plumbing
+
+    @property
+    def space(self) -> DeviceSpace:
+        return self.group.device_space
+
+    @property
+    def gpu(self) -> int:
+        return self.group.gpu_of(self.id)
+
+    @property
+    def stream(self) -> torch.cuda.Stream:
+        return self.space.stream_of(self.id)
+
+    def connect(self, peer: int, address: str | None = None) -> Endpoint:
+        ep = self.endpoints.get(peer)
+        if ep is None:
+            if peer not in self.group.workers:
+                raise TransportError(f"no worker {peer} in this group")
+            ep = self.endpoints[peer] = Endpoint(self, peer)
+        return ep
+
+    def _fire(self, handle, comp: Completion) -> None:
+        self._fired.append((handle, comp))
+
+    def _after(self, event, fn) -> None:
+        self._inflight.append(_Inflight(event, fn))
+
+    # ---------------------------------------------------------------- sends
+
+    def tag_send(self, ep: Endpoint, tag: int, payload, completion=None, length=None) -> None:
+        """Non-blocking tagged send (cl/transport.py:258-295)."""
+        if not 0 <= tag <= FULL_MASK:
+            raise ValueError(f"tag 0x{tag:x} outside 64 bits")
+        if ep.failed:
+            self._fire(completion, Completion(status=TRANSPORT_ERROR, tag=tag,
+                                              error=f"endpoint to {ep.peer} failed"))
+            return
+        if _is_device(payload):
+            source = as_region(payload, length)
+            nbytes = source.size
+        else:
+            data = bytes(payload)
+            if length is not None:
+                if length > len(data):
+                    raise ValueError(f"length {length} exceeds payload of {len(data)}")
+                data = data[:length]
+            source, nbytes = data, len(data)
+        if nbytes > self.cfg.max_message_bytes:
+            raise ValueError(f"payload of {nbytes} bytes exceeds max message size "
+                             f"{self.cfg.max_message_bytes}")
+        peer = self.group.workers[ep.peer]
+        if nbytes <= self.cfg.eager_threshold:
+            ready, keep = None, None
+            if isinstance(source, DeviceRegion):
+                source, ready, keep = self._snapshot(source)
+            frame = Frame(FRAME_EAGER, tag, nbytes, source, ready, self.id, keepalive=keep)
+            self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
+        else:
+            ready = None
+            if isinstance(source, DeviceRegion):
+                ready = torch.cuda.Event()
+                ready.record(self.space.stream_of(source.buffer.owner))
+            frame = Frame(FRAME_RTS, tag, nbytes, source, ready, self.id, send_completion=completion)
+        self.stats[f"tx_{_NAMES[frame.kind]}"] += 1
+        self.stats["sends"] += 1
+        peer.inbound.append(frame)
+
+    def _snapshot(self, src: DeviceRegion):
+        """Stream-ordered copy of an eager device payload into a bounce buffer."""
+        buf = src.buffer
+        s = self.space.stream_of(buf.owner)
+        with torch.cuda.stream(s):
+            bounce = torch.empty(max(src.size, 1), dtype=torch.uint8, device=f"cuda:{buf.gpu}")
+        _lib.call("hx_set_device", buf.gpu)
+        if src.size:
+            _lib.call("hx_memcpy", bounce.data_ptr(), src.addr, src.size, s.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        return _Bounce(bounce, src.size, buf.gpu, buf.owner), ev, bounce
+
+    # ------------------------------------------------------------- receives
+
+    def tag_recv(self, tag: int, mask: int = FULL_MASK, capacity: int = 0,
+                 completion=None, sink=None) -> ReceiveRequest:
+        """Post a tagged receive; matches queued unexpected frames first."""
+        return self._post(tag, mask, capacity, sink, completion, wildcard=False)
+
+    def _post(self, tag, mask, capacity, sink, completion, wildcard) -> ReceiveRequest:
+        req = ReceiveRequest(tag, mask, capacity, sink, completion, self._post_seq, wildcard)
+        self._post_seq += 1
+        for i, frame in enumerate(self.unexpected):
+            if req.matches(frame.tag):
+                del self.unexpected[i]
+                self._absorb(req, frame)
+                return req
+        self.posted.append(req)
+        return req
+
+    def tag_probe(self, tag: int, mask: int = FULL_MASK):
+        for frame in self.unexpected:
+            if (frame.tag & mask) == (tag & mask):
+                return frame.tag, frame.length
+        return None
+
+    # ------------------------------------------------------------- progress
+
+    def progress(self) -> int:
+        """Drain arrivals, poll GPU copies, fire completions (cl/transport.py:342-362)."""
+        while self.inbound:
+            frame = self.inbound.popleft()
+            if self.hold is not None and self.hold(frame):
+                self._held.append(frame)
+                continue
+            self._arrived(frame)
+        if self._inflight:
+            pending = []
+            for op in self._inflight:
+                if op.event.query():
+                    op.fn()
+                else:
+                    pending.append(op)
+            self._inflight = pending
+        fired = 0
+        while self._fired:
+            handle, comp = self._fired.popleft()
+            if comp.timestamp is None:
+                comp.timestamp = self.clock.now
+            fired += 1
+            if handle is not None:
+                deliver(handle, comp)
+        self.stats["completions"] += fired
+        return fired
+
+    def release_held(self) -> None:
+        self.inbound.extendleft(reversed(self._held))
+        self._held.clear()
+
+    @property
+    def idle(self) -> bool:
+        """No arrivals, completions, or in-flight GPU copies."""
+        return not (self.inbound or self._fired or self._inflight)
+
+    def _arrived(self, frame: Frame) -> None:
+        frame.seq = self._arrival_seq
+        self._arrival_seq += 1
+        self.stats[f"rx_{_NAMES[frame.kind]}"] += 1
+        for i, req in enumerate(self.posted):
+            if req.matches(frame.tag):
+                del self.posted[i]
+                self._absorb(req, frame)
+                return
+        self.unexpected.append(frame)
+
+    def _absorb(self, req: ReceiveRequest, frame: Frame) -> None:
+        """A request met a frame: move the bytes or truncate."""
+        sender = self.group.workers[frame.src]
+        if frame.length > req.capacity:
+            self._fire(req.completion, Completion(
+                status=TRUNCATED, length=frame.length, tag=frame.tag,
+                error=f"frame of {frame.length} bytes exceeds capacity {req.capacity}"))
+            if frame.kind == FRAME_RTS:  # the reference serves the pull anyway
+                sender._fire(frame.send_completion, Completion(status=OK, length=frame.length,
+                                                               tag=frame.tag))
+            return
+        try:
+            self._move(req, frame, sender)
+        except Exception as e:  # CUDA failure -> transport-error statuses
+            err = Completion(status=TRANSPORT_ERROR, tag=frame.tag, error=repr(e))
+            self._fire(req.completion, err)
+            if frame.kind == FRAME_RTS:
+                sender._fire(frame.send_completion, err)
+
+    def _move(self, req: ReceiveRequest, frame: Frame, sender: "Worker") -> None:
+        src, n, sink = frame.source, frame.length, req.sink
+        if isinstance(sink, DeviceBuffer):
+            sink = sink.region()
+
+        def done(payload=None):
+            comp = Completion(status=OK, length=n, tag=frame.tag, payload=payload)
+            if req.wildcard:
+                self._post(req.tag, req.mask, req.capacity, None, None, wildcard=True)
+                if self.eager_handler is not None:
+                    self.eager_handler(frame.tag, payload, self.clock.now)
+                else:
+                    self.eager_inbox.append((frame.tag, payload, self.clock.now))
+                return
+            self._fire(req.completion, comp)
+
+        def send_done():
+            if frame.kind == FRAME_RTS:
+                sender._fire(frame.send_completion, Completion(status=OK, length=n, tag=frame.tag))
+
+        if isinstance(src, bytes):
+            if isinstance(sink, DeviceRegion):  # host -> device (pinned H2D)
+                ev = self._h2d(sink, src)
+                self._after(ev, done)
+                send_done()
+            elif sink is None:
+                done(src)
+                send_done()
+            else:
+                sink[:n] = src
+                done()
+                send_done()
+            return
+        # device source: the sender's region (rdv) or a bounce snapshot (eager)
+        if isinstance(sink, DeviceRegion):
+            ev = self._d2d(sink, src, n, frame.ready)
+            keep = frame.keepalive
+
+            def landed(keep=keep):
+                done()
+                send_done()
+
+            self._after(ev, landed)
+            if frame.kind == FRAME_RTS:
+                sender._after(ev, lambda: None)  # sender stays non-idle until the read ends
+        else:
+            ev, stage = self._d2h(src, n, frame.ready)
+
+            def landed_host(stage=stage, keep=frame.keepalive):
+                data = stage.numpy()[:n].tobytes()
+                if sink is None:
+                    done(data)
+                else:
+                    sink[:n] = data
+                    done()
+                send_done()
+
+            self._after(ev, landed_host)
+
+    # ----------------------------------------------------------- GPU copies
+
+    def _d2d(self, dst: DeviceRegion, src, n: int, ready):
+        """Direct HBM / NVLink peer copy on the sink owner's stream."""
+        owner = dst.buffer.owner
+        s = self.space.stream_of(owner)
+        if ready is not None:
+            s.wait_event(ready)
+        _lib.call("hx_set_device", dst.buffer.gpu)
+        if n:
+            _lib.call("hx_memcpy", dst.addr, src.addr, n, s.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        self.stats["d2d_copies"] += 1
+        self.stats["d2d_bytes"] += n
+        return ev
+
+    def _h2d(self, dst: DeviceRegion, data: bytes):
+        s = self.space.stream_of(dst.buffer.owner)
+        stage = torch.empty(max(len(data), 1), dtype=torch.uint8, pin_memory=True)
+        stage.numpy()[: len(data)] = np.frombuffer(data, dtype=np.uint8)
+        _lib.call("hx_set_device", dst.buffer.gpu)
+        if data:
+            _lib.call("hx_memcpy", dst.addr, stage.data_ptr(), len(data), s.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        self._after(ev, lambda stage=stage: None)  # keep the staging alive until landed
+        return ev
+
+    def _d2h(self, src, n: int, ready):
+        gpu = src.gpu if isinstance(src, _Bounce) else src.buffer.gpu
+        owner = src.owner if isinstance(src, _Bounce) else src.buffer.owner
+        s = self.space.stream_of(owner)
+        if ready is not None:
+            s.wait_event(ready)
+        stage = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
+        _lib.call("hx_set_device", gpu)
+        if n:
+            _lib.call("hx_memcpy", stage.data_ptr(), src.addr, n, s.cuda_stream)
+        ev = torch.cuda.Event()
+        ev.record(s)
+        return ev, stage
+
+    def close(self) -> None:
+        pass
+
+
+class _Bounce:
+    """Device snapshot of an eager payload (owned by the transport)."""
+
+    __slots__ = ("t", "addr", "size", "gpu", "owner")
+
+    def __init__(self, t, size, gpu, owner):
+        self.t = t
+        self.addr = t.data_ptr()
+        self.size = size
+        self.gpu = gpu
+        self.owner = owner
+
+
+class TransportGroup:
+    """Process-local workers, wall clocks and the HBM device space
+    (cl/transport.py:601-636). Enables NVLink peer access between every
+    pair of GPUs the workers use."""
+
+    def __init__(self, cfg: RuntimeConfig | None = None, backend: str = "loopback"):
+        if backend != "loopback":
+            raise StartupError(f"backend {backend!r} is out of scope on the B200 path "
+                               "(single box, NVLink); use 'loopback'")
+        self.cfg = cfg or RuntimeConfig()
+        self.backend = backend
+        self.layout = TagLayout.from_spec(self.cfg.tag_layout)
+        self.workers: dict[int, Worker] = {}
+        self.clocks: dict[int, WallClock] = {}
+        self._device_space: DeviceSpace | None = None
+        self._ngpu = None
+
+    def gpu_of(self, worker: int) -> int:
+        if self.cfg.gpus:
+            return int(self.cfg.gpus[worker % len(self.cfg.gpus)])
+        if self._ngpu is None:
+            self._ngpu = max(1, torch.cuda.device_count())
+        return worker % self._ngpu
+
+    def create_worker(self, worker_id: int, listen: str | None = None) -> Worker:
+        if worker_id in self.workers:
+            raise StartupError(f"duplicate worker id {worker_id} in process group")
+        self.clocks[worker_id] = WallClock()
+        w = Worker(self, worker_id)
+        self.workers[worker_id] = w
+        return w
+
+    @property
+    def device_space(self) -> DeviceSpace:
+        if self._device_space is None:
+            self._device_space = DeviceSpace(self.gpu_of, self.clocks, self.cfg.device_capacity)
+            gpus = sorted({self.gpu_of(w) for w in range(max(self.cfg.workers, 1))})
+            for a in gpus:
+                for b in gpus:
+                    if a != b:
+                        ok = ctypes.c_int(0)
+                        _lib.call("hx_can_access_peer", a, b, ctypes.byref(ok))
+                        if ok.value:
+                            _lib.call("hx_enable_peer", a, b)
+        return self._device_space
+
+    def close(self) -> None:
+        if self._device_space is not None:
+            for s in self._device_space._streams.values():
+                s.synchronize()

@@ -1,0 +1,98 @@
+"""CPU-only checks: the C-ABI library loads and exports every symbol
+include/hx.h declares; host-side logic (tags, config, decomposition,
+neighbour tables, arena layout, size parsing) matches the reference's
+golden vectors. No compute calls (no GPU here)."""
+
+import ctypes
+import json
+import os
+import re
+
+import pytest
+
+from paper_2102_12416_b200 import _lib
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+GOLD = json.load(open(os.path.join(ROOT, "tests", "golden", "golden.json")))
+
+
+def test_library_exports_every_declared_symbol():
+    header = open(os.path.join(ROOT, "include", "hx.h")).read()
+    declared = set(re.findall(r"^\s*(?:int|const char \*)\s*(hx_\w+)\s*\(", header, re.M))
+    assert declared == set(_lib.EXPORTS)
+    lib = ctypes.CDLL(_lib.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert _lib.load().hx_abi_version() == 1
+    assert _lib.error_string(-2) == "hx: device flag wait timed out"
+
+
+def test_library_is_sm100a_only():
+    import subprocess
+
+    out = subprocess.run(["cuobjdump", "--list-elf", _lib.LIB_PATH], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+    sass = subprocess.run(["cuobjdump", "-sass", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "UTMALDG" in sass  # the stencil stages planes with TMA
+
+
+def test_tag_codec_matches_reference():
+    from paper_2102_12416_b200.tags import TagLayout
+
+    lay = TagLayout()
+    for cid, d, c, want in GOLD["tags"]["channel"]:
+        assert lay.encode_channel(cid, d, c) == want
+        dec = lay.decode(want)
+        assert (dec.channel_id, dec.direction, dec.counter) == (cid, d, c)
+    for kind, pe, c, want in GOLD["tags"]["messaging"]:
+        assert lay.encode_messaging(kind, pe, c) == want
+    assert lay.digest() == GOLD["tags"]["digest"]
+
+
+def test_decompose_neighbors_match_reference():
+    from paper_2102_12416_b200.jacobi3d import JacobiError, decompose, neighbor_table
+
+    for key, want in GOLD["decompose"].items():
+        dims_s, n = key.rsplit("/", 1)
+        dims = tuple(int(x) for x in dims_s.strip("()").split(","))
+        if want is None:
+            with pytest.raises(JacobiError):
+                decompose(dims, int(n))
+        else:
+            assert list(decompose(dims, int(n))) == want, key
+    for g_s, tables in GOLD["neighbors"].items():
+        grid = tuple(int(x) for x in g_s.strip("()").split(","))
+        for r, want in enumerate(tables):
+            assert neighbor_table(grid, r) == want
+
+
+def test_b200_policy_keeps_area_and_avoids_z():
+    from paper_2102_12416_b200.jacobi3d import decompose, decompose_b200, internal_face_area
+
+    for dims in ((64, 64, 64), (128, 64, 64), (3072, 3072, 3072), (96, 48, 24)):
+        for n in (1, 2, 4, 8, 16):
+            try:
+                a, b = decompose(dims, n), decompose_b200(dims, n)
+            except Exception:
+                continue
+            assert internal_face_area(dims, a) == internal_face_area(dims, b)
+    assert decompose((64, 64, 64), 2) == (1, 1, 2)       # reference: splits z
+    assert decompose_b200((64, 64, 64), 2) == (2, 1, 1)  # B200: splits x instead
+
+
+def test_config_rejects_virtual_time():
+    from paper_2102_12416_b200.config import ConfigError, RuntimeConfig
+
+    with pytest.raises(ConfigError):
+        RuntimeConfig(time_mode="virtual")
+    assert RuntimeConfig().time_mode == "wall"
+
+
+def test_parse_sizes():
+    from paper_2102_12416_b200.osu import BenchError, parse_sizes
+
+    assert parse_sizes("1:4194304:x2")[-1] == 4194304 and len(parse_sizes("8:4194304:x2")) == 20
+    assert parse_sizes("8,64,4096") == [8, 64, 4096]
+    assert parse_sizes("1:10:+4") == [1, 5, 9]
+    with pytest.raises(BenchError):
+        parse_sizes("1:10:y2")

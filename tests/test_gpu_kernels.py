@@ -1,0 +1,223 @@
+"""GPU parity of the libhx kernels against the CPU oracle (bit-exact).
+
+Calls the C ABI (include/hx.h) through paper_2102_12416_b200._lib on
+seeded inputs: the 6-neighbour stencil (TMA and generic variants, odd and
+even extents, sub-boxes), the fused residual, face pack/unpack in all six
+directions, the fused pack+put+signal / wait+unpack pair, and the
+sequential 64^3 x 100 golden run of the reference.
+"""
+
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import jacobi_c, jacobi_np  # noqa: E402
+
+GOLD_DIR = os.path.join(os.path.dirname(__file__), "golden")
+GOLD = json.load(open(os.path.join(GOLD_DIR, "golden.json")))
+ARR = np.load(os.path.join(GOLD_DIR, "golden.npz"))
+
+SHAPES = [(1, 1, 1), (2, 3, 4), (8, 6, 10), (6, 14, 11), (16, 16, 16), (33, 47, 64),
+          (20, 70, 130), (64, 64, 64), (5, 40, 258)]
+
+
+@pytest.fixture(scope="module")
+def hx(cuda):
+    from paper_2102_12416_b200 import _lib
+
+    _lib.call("hx_set_device", 0)
+    yield _lib
+    _lib.raw("hx_stencil_set_variant")(0)
+
+
+def stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def run_stencil(hx, cur, variant, res=False, box=None):
+    bx, by, bz = (s - 2 for s in cur.shape)
+    rng = np.random.default_rng(99)
+    nxt0 = rng.standard_normal(cur.shape)  # ghosts must survive untouched
+    c, n = dev(cur), dev(nxt0)
+    r = torch.zeros(1, dtype=torch.int64, device="cuda")
+    hx.raw("hx_stencil_set_variant")(variant)
+    rp = r.data_ptr() if res else None
+    if box is None:
+        hx.call("hx_stencil", c.data_ptr(), n.data_ptr(), bx, by, bz, rp, stream())
+    else:
+        hx.call("hx_stencil_box", c.data_ptr(), n.data_ptr(), bx, by, bz, *box, rp, stream())
+    torch.cuda.synchronize()
+    return nxt0, n.cpu().numpy(), float(r.cpu().numpy().view(np.float64)[0])
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("variant", [0, 2])
+def test_stencil_bitexact_vs_oracle(hx, shape, variant):
+    rng = np.random.default_rng(sum(shape))
+    cur = rng.standard_normal(tuple(s + 2 for s in shape))
+    nxt0, got, res = run_stencil(hx, cur, variant, res=True)
+    want = nxt0.copy()
+    wres = jacobi_c.stencil_residual(cur, want, nthreads=2)
+    assert got.tobytes() == want.tobytes()
+    assert res == wres
+    if variant == 0 and (shape[2] + 2) % 2 == 0:
+        assert hx.raw("hx_stencil_last_variant")() == 1  # the TMA pipeline ran
+
+
+def test_tma_forced_on_even_z(hx):
+    rng = np.random.default_rng(5)
+    cur = rng.standard_normal((40, 36, 66))
+    nxt0, got, _ = run_stencil(hx, cur, 1)
+    want = nxt0.copy()
+    jacobi_np.stencil(cur, want)
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("chunk", [1, 3, 7, 1000])
+def test_tma_chunking_is_invisible(hx, chunk):
+    rng = np.random.default_rng(chunk)
+    cur = rng.standard_normal((31, 40, 70))
+    hx.raw("hx_stencil_set_chunk")(chunk)
+    try:
+        nxt0, got, res = run_stencil(hx, cur, 1, res=True)
+    finally:
+        hx.raw("hx_stencil_set_chunk")(0)
+    want = nxt0.copy()
+    assert res == jacobi_c.stencil_residual(cur, want)
+    assert got.tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_box_plus_shells_equal_full_sweep(hx, variant):
+    """Interior box + six boundary slabs (the overlap split) == one sweep."""
+    rng = np.random.default_rng(11)
+    cur = rng.standard_normal((22, 36, 68))
+    bx, by, bz = 20, 34, 66
+    inner = (2, bx, 2, by, 2, bz)
+    slabs = [(1, 2, 1, by + 1, 1, bz + 1), (bx, bx + 1, 1, by + 1, 1, bz + 1),
+             (2, bx, 1, 2, 1, bz + 1), (2, bx, by, by + 1, 1, bz + 1),
+             (2, bx, 2, by, 1, 2), (2, bx, 2, by, bz, bz + 1)]
+    c = dev(cur)
+    nxt0 = rng.standard_normal(cur.shape)
+    n = dev(nxt0)
+    for box in [inner] + slabs:
+        hx.raw("hx_stencil_set_variant")(variant if box is inner else 2)
+        hx.call("hx_stencil_box", c.data_ptr(), n.data_ptr(), bx, by, bz, *box, None, stream())
+    hx.raw("hx_stencil_set_variant")(0)
+    want = nxt0.copy()
+    jacobi_np.stencil(cur, want)
+    assert n.cpu().numpy().tobytes() == want.tobytes()
+
+
+def test_sequential_64_cubed_matches_reference_golden(hx):
+    from paper_2102_12416_b200.jacobi3d import sequential_oracle
+
+    field, res = sequential_oracle((64, 64, 64), 100)
+    g = GOLD["seq_64_100"]
+    assert hashlib.sha256(field.tobytes()).hexdigest() == g["sha256"]
+    assert [r.hex() for r in res] == g["residuals_hex"]
+
+
+def test_sequential_custom_boundaries(hx):
+    from paper_2102_12416_b200.jacobi3d import sequential_oracle
+
+    f, _ = sequential_oracle((12, 10, 14), 7, hot=0.75, background=0.125, fill=0.5)
+    assert f.tobytes() == ARR["seq_12x10x14_7_custom"].tobytes()
+
+
+@pytest.mark.parametrize("tag", ["a", "b", "c"])
+def test_pack_unpack_match_reference_fixtures(hx, tag):
+    meta = GOLD[f"block_{tag}"]
+    field = ARR[f"pack_{tag}_field"]
+    bx, by, bz = (s - 2 for s in field.shape)
+    f = dev(field)
+    for d in meta["nbr_dirs"]:
+        want = ARR[f"pack_{tag}_face{d}"]
+        out = torch.full((want.size,), float("nan"), dtype=torch.float64, device="cuda")
+        hx.call("hx_pack", f.data_ptr(), bx, by, bz, d, out.data_ptr(), stream())
+        assert out.cpu().numpy().tobytes() == want.tobytes()
+    for d in meta["nbr_dirs"]:
+        face = dev(ARR[f"unpack_{tag}_rstage{d}"])
+        hx.call("hx_unpack", f.data_ptr(), bx, by, bz, d, face.data_ptr(), stream())
+    assert f.cpu().numpy().tobytes() == ARR[f"unpack_{tag}_field"].tobytes()
+
+
+@pytest.mark.parametrize("shape", [(3, 4, 5), (17, 9, 130), (64, 64, 64), (2, 2100, 3)])
+def test_pack_unpack_all_dirs_random(hx, shape):
+    rng = np.random.default_rng(len(shape) + sum(shape))
+    field = rng.standard_normal(tuple(s + 2 for s in shape))
+    f = dev(field)
+    for d in range(6):
+        want = jacobi_np.pack_face(field, d)
+        out = torch.empty(want.size, dtype=torch.float64, device="cuda")
+        hx.call("hx_pack", f.data_ptr(), *shape, d, out.data_ptr(), stream())
+        assert out.cpu().numpy().tobytes() == want.tobytes(), d
+        face = rng.standard_normal(want.shape)
+        ref = field.copy()
+        jacobi_np.unpack_face(ref, d, face)
+        g = dev(field)
+        hx.call("hx_unpack", g.data_ptr(), *shape, d, dev(face).data_ptr(), stream())
+        assert g.cpu().numpy().tobytes() == ref.tobytes(), d
+
+
+def test_fused_pack_put_wait_unpack_roundtrip(hx):
+    """Two blocks on one stream: puts (with flag release) then waits."""
+    import ctypes
+
+    rng = np.random.default_rng(3)
+    shape = (12, 10, 16)
+    a = rng.standard_normal(tuple(s + 2 for s in shape))
+    slots = torch.zeros(6 * 4096, dtype=torch.float64, device="cuda")
+    flags = torch.zeros(8, dtype=torch.int64, device="cuda")
+    ctr = torch.zeros(8, dtype=torch.int32, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    fa = dev(a)
+    V = ctypes.c_void_p * 6
+    dst = V(*[slots.data_ptr() + 8 * 4096 * d for d in range(6)])
+    flg = V(*[flags.data_ptr() + 8 * d for d in range(6)])
+    hx.call("hx_pack_put", fa.data_ptr(), *shape, 0b111111, dst, flg, 7, ctr.data_ptr(), stream())
+    b = rng.standard_normal(a.shape)
+    fb = dev(b)
+    hx.call("hx_wait_unpack", fb.data_ptr(), *shape, 0b111111, dst, flg, 7, int(5e9),
+            err.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert int(err.item()) == 0
+    assert flags.cpu().numpy()[:6].tolist() == [7] * 6
+    assert ctr.cpu().numpy()[:6].tolist() == [0] * 6  # counters re-armed
+    ref = b.copy()
+    for d in range(6):
+        jacobi_np.unpack_face(ref, d, jacobi_np.pack_face(a, d))
+    assert fb.cpu().numpy().tobytes() == ref.tobytes()
+
+
+def test_wait_times_out_instead_of_hanging(hx):
+    flags = torch.zeros(1, dtype=torch.int64, device="cuda")
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    hx.call("hx_wait_flag", flags.data_ptr(), 1, int(2e7), err.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert int(err.item()) == -2  # HX_E_TIMEOUT
+
+
+def test_medium_block_vs_threaded_c_oracle(hx):
+    """A 190 x 200 x 390 block (partial TMA tiles in j and k) over 3 sweeps."""
+    rng = np.random.default_rng(17)
+    cur = rng.standard_normal((192, 202, 392))
+    c, n = dev(cur), dev(cur)
+    h_cur, h_nxt = cur.copy(), cur.copy()
+    for _ in range(3):
+        hx.call("hx_stencil", c.data_ptr(), n.data_ptr(), 190, 200, 390, None, stream())
+        c, n = n, c
+        jacobi_c.stencil(h_cur, h_nxt)
+        h_cur, h_nxt = h_nxt, h_cur
+    assert c.cpu().numpy().tobytes() == h_cur.tobytes()
