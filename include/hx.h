@@ -102,6 +102,10 @@ int hx_stencil_set_variant(int variant);
 int hx_stencil_last_variant(void);
 /* Tuning knob for the TMA pipeline: x planes per CTA work item (0 = auto). */
 int hx_stencil_set_chunk(int planes);
+/* Self-check of the stencil's division by 6 (RN(1/6) product + one FMA
+ * correction, Markstein) against the library's correctly rounded __ddiv_rn
+ * over n device doubles; *mismatches (device u64, caller-zeroed) += count. */
+int hx_div6_check(const double *in, size_t n, unsigned long long *mismatches, void *stream);
 
 /* Hot-wall / Dirichlet initialisation of one padded block
  * (cl/jacobi3d.py:135-138, 186-188): every cell = background, interior =

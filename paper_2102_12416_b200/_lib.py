@@ -30,7 +30,7 @@ EXPORTS = (
     "hx_malloc", "hx_free", "hx_malloc_host", "hx_free_host", "hx_can_access_peer",
     "hx_enable_peer", "hx_ipc_get", "hx_ipc_open", "hx_ipc_close", "hx_memcpy",
     "hx_memcpy_peer", "hx_copy_sm", "hx_fill_f64", "hx_stencil", "hx_stencil_box",
-    "hx_stencil_set_variant", "hx_stencil_last_variant", "hx_stencil_set_chunk",
+    "hx_stencil_set_variant", "hx_stencil_last_variant", "hx_stencil_set_chunk", "hx_div6_check",
     "hx_init_block", "hx_pack", "hx_unpack", "hx_pack_put", "hx_wait_unpack", "hx_signal",
     "hx_wait_flag", "hx_read_u64", "hx_pingpong",
 )
@@ -94,6 +94,7 @@ _SIGS = {
     "hx_stencil_set_variant": ([_I], _I),
     "hx_stencil_last_variant": ([], _I),
     "hx_stencil_set_chunk": ([_I], _I),
+    "hx_div6_check": ([_V, _SZ, _V, _V], _I),
     "hx_init_block": ([_V, _I, _I, _I, _I, _D, _D, _D, _V], _I),
     "hx_pack": ([_V, _I, _I, _I, _I, _V, _V], _I),
     "hx_unpack": ([_V, _I, _I, _I, _I, _V, _V], _I),

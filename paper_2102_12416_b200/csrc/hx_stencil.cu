@@ -4,26 +4,35 @@
 // oracle's identical sweep + residual, 192-198):
 //   nxt[i,j,k] = (((((c[i-1,j,k] + c[i+1,j,k]) + c[i,j-1,k]) + c[i,j+1,k])
 //                 + c[i,j,k-1]) + c[i,j,k+1]) / 6.0
-// The adds are issued in exactly this order and the division is the IEEE
-// correctly rounded div.rn.f64 (never a multiply by 1/6), so results are
+// The adds are issued in exactly this order (no contraction) and the
+// quotient is the IEEE correctly rounded t / 6.0, so results are
 // bit-identical to numpy. Ghost cells of nxt are never written.
+//
+// Division by 6 (div6): y = RN(1/6) = 0x3FC5555555555555 has relative error
+// 2^-54, so q = RN(t*y) is within 1 ulp of t/6; with the exact FMA remainder
+// r = t - 6q, Markstein's theorem gives RN(q + r*y) = RN(t/6) for every t
+// whose intermediate values stay normal. Zero, subnormal-range, huge and
+// non-finite sums take the library __ddiv_rn. 3 FP64 ops instead of the
+// generic divide's ~20 + branch; hx_div6_check verifies it on device.
 //
 // Primary kernel (HBM-bound, 16 algorithmic bytes per cell): a 2.5-D
 // streaming sweep. Each CTA owns a TY x TZ tile of the (j,k) plane and
 // marches along x (the slowest axis) over a chunk of planes. Every padded
-// plane tile (TY+2) x (TZ+2) is fetched exactly once by a TMA bulk-tensor
-// load into an S-stage shared-memory ring guarded by mbarriers, so each
-// input cell crosses HBM once (plus the thin tile halos, which L2 serves);
-// the x-neighbours come from the adjacent ring stages and the y/z
-// neighbours from the current stage. Outputs are stored straight from
-// registers with coalesced 8-byte stores. The residual max|nxt-cur| reuses
-// the centre value already in shared memory (no extra traffic) and is
-// reduced warp -> CTA -> one atomicMax on the uint64 bit pattern (valid
-// for non-negative doubles).
+// plane tile (TY+2) x (TZ+4) is fetched once by a TMA bulk-tensor load into
+// an NS-stage shared-memory ring guarded by mbarriers; each input cell
+// crosses HBM once (tile halos are served by L2 — ncu: 59.0 GB DRAM for
+// 58.0 GB algorithmic at 1536^3). Each thread keeps its columns' x-1 and x
+// values in registers (register marching), so per cell it reads only the
+// x+1 centre and the four y/z neighbours from shared memory. Outputs are
+// stored from registers with coalesced stores through pointers advanced
+// one plane per step. The residual max|nxt-cur| uses the register-resident
+// centre and is reduced warp -> CTA -> one atomicMax on the uint64 bit
+// pattern (valid for non-negative doubles).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -33,29 +42,59 @@
 
 namespace {
 
-constexpr int TY = 32;           // tile rows (j)
-constexpr int TZ = 64;           // tile columns (k)
-constexpr int NSTAGE = 6;        // shared-memory ring depth (planes)
-constexpr int THREADS = 256;     // 8 warps; warp w owns rows w, w+8, w+16, w+24
-constexpr int ROWS_PER_WARP = TY / (THREADS / 32);
-constexpr int BOX_Y = TY + 2, BOX_Z = TZ + 2;
-constexpr unsigned STAGE_BYTES = BOX_Y * BOX_Z * sizeof(double);             // 17952
-constexpr unsigned STAGE_STRIDE = (STAGE_BYTES + 127) / 128 * 128;           // TMA: 128 B aligned
+constexpr int TY = 32;        // tile rows (j)
+constexpr int TZ = 64;        // tile columns (k): two 32-lane halves
+constexpr int NSTAGE = 4;     // shared-memory ring depth (planes)
+constexpr int MIN_CTAS = 3;   // resident CTAs per SM (smem: 3 x 74 KB)
+constexpr int THREADS = 256;  // 8 warps; warp w owns rows w, w+8, w+16, w+24
+constexpr int NWARP = THREADS / 32;
+constexpr int ROWS = TY / NWARP;
+constexpr int PTS = ROWS * 2;  // cells per thread per plane
+// A box row is TZ+2 doubles (the tile plus its z halo). TMA only accepts
+// 16-byte aligned row starts, so when the tile's first input column kb-1 is
+// odd (sub-box sweeps starting at an even k) the load starts one element
+// earlier and the box is TZ+4 wide (kshift = 1). Full sweeps use TZ+2.
+constexpr int BOX_Y = TY + 2, BOX_Z_MAX = TZ + 4;
+constexpr unsigned STAGE_STRIDE = (BOX_Y * BOX_Z_MAX * sizeof(double) + 127) / 128 * 128;
 constexpr size_t SMEM_BYTES = (size_t)NSTAGE * STAGE_STRIDE + NSTAGE * sizeof(uint64_t);
 
-int g_variant = 0;     // 0 auto, 1 TMA, 2 generic
+int g_variant = 0;  // 0 auto, 1 TMA, 2 generic
 int g_last_variant = 0;
-int g_chunk = 0;       // planes per CTA work item, 0 = auto
+int g_chunk = 0;  // planes per CTA work item, 0 = auto
 int g_num_sms = 0;
+int g_l2promo = -1;  // CUtensorMapL2promotion for the plane loads; -1 = default
 
-__device__ __forceinline__ double relax(double xm, double xp, double ym, double yp, double zm,
-                                        double zp) {
+constexpr double RCP6 = 0.16666666666666666;  // RN(1/6) = 0x3FC5555555555555
+
+// +0.0 is exact on the fast path (q = r = +0) and is by far the most common
+// sum early in a hot-wall run, so it must not take the slow path; -0.0
+// would come out as +0.0 and goes to the library division.
+__device__ __forceinline__ bool div6_fast_ok(double t) {
+    const double a = fabs(t);
+    return (a >= 0x1p-960 && a <= 0x1p1020) || __double_as_longlong(t) == 0;
+}
+
+__device__ __forceinline__ double div6_fast(double t) {
+    const double q = __dmul_rn(t, RCP6);
+    const double r = __fma_rn(-6.0, q, t);
+    return __fma_rn(r, RCP6, q);
+}
+
+__device__ __noinline__ double div6_slow(double t) {
+    return t == 0.0 ? t : __ddiv_rn(t, 6.0);
+}
+
+__device__ __forceinline__ double div6(double t) {
+    return div6_fast_ok(t) ? div6_fast(t) : div6_slow(t);
+}
+
+__device__ __forceinline__ double sum6(double xm, double xp, double ym, double yp, double zm,
+                                       double zp) {
     double t = __dadd_rn(xm, xp);
     t = __dadd_rn(t, ym);
     t = __dadd_rn(t, yp);
     t = __dadd_rn(t, zm);
-    t = __dadd_rn(t, zp);
-    return __ddiv_rn(t, 6.0);
+    return __dadd_rn(t, zp);
 }
 
 __device__ __forceinline__ void cta_max_to_global(double worst, unsigned long long *res) {
@@ -76,79 +115,121 @@ __device__ __forceinline__ void cta_max_to_global(double worst, unsigned long lo
 // ------------------------------------------------------- TMA pipeline ----
 // Work item = (tile j, tile k, x chunk). Box in interior coordinates:
 // [i0,i1) x [j0,j1) x [k0,k1).
-__global__ void __launch_bounds__(THREADS, 2)
+template <bool RES, int BOX_Z>
+__global__ void __launch_bounds__(THREADS, MIN_CTAS)
 stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__ nxt, int by,
                    int bz, int i0, int i1, int j0, int j1, int k0, int k1, int ntj, int ntk,
-                   int chunk, unsigned long long *res) {
+                   int chunk, int nchunks, int grows, unsigned long long *res) {
+    constexpr unsigned STAGE_BYTES = BOX_Y * BOX_Z * sizeof(double);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
 
-    int item = blockIdx.x;
-    const int tk = item % ntk;
-    item /= ntk;
-    const int tj = item % ntj;
-    const int c = item / ntj;
+    // Work order: groups of `grows` tile rows; inside a group all tiles of
+    // chunk c, then chunk c+1, ... Concurrent CTAs therefore cover adjacent
+    // tiles of the same few planes (tile halos hit L2) and chunk c+1 of a
+    // tile starts while chunk c's last planes are still in L2.
+    const int items_g = grows * ntk * nchunks;
+    const int g = blockIdx.x / items_g;
+    const int rem = blockIdx.x - g * items_g;
+    const int tiles_g = min(grows, ntj - g * grows) * ntk;
+    const int c = rem / tiles_g;
+    const int t = rem - c * tiles_g;
+    const int tj = g * grows + t / ntk;
+    const int tk = t % ntk;
     const int jb = j0 + tj * TY, kb = k0 + tk * TZ;
     const int ib = i0 + c * chunk;
     const int ie = min(ib + chunk, i1);
     const int nplanes = ie - ib + 2;  // padded planes ib-1 .. ie
+    const int kshift = BOX_Z == TZ + 2 ? 0 : (kb - 1) & 1;  // 16-byte aligned TMA rows
+    const int kload = kb - 1 - kshift;
 
     if (threadIdx.x == 0) {
         hx::prefetch_tmap(&map);
         for (int s = 0; s < NSTAGE; ++s) hx::mbar_init(&bar[s], 1);
         hx::fence_mbar_init();
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
         const int pre = min(NSTAGE, nplanes);
         for (int p = 0; p < pre; ++p) {
             hx::mbar_expect_tx(&bar[p], STAGE_BYTES);
-            hx::tma_load_3d(smem + p * STAGE_STRIDE, &map, kb - 1, jb - 1, ib - 1 + p, &bar[p]);
+            hx::tma_load_3d(smem + p * STAGE_STRIDE, &map, kload, jb - 1, ib - 1 + p, &bar[p]);
         }
     }
+    __syncthreads();
 
-    const hx::Geom g(by, bz);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    bool kok[2];
+    // shared-memory offset (doubles) of this thread's first cell centre
+    const int soff = (warp + 1) * BOX_Z + lane + 1 + kshift;
+    const size_t plane = (size_t)(by + 2) * (bz + 2);
+    double *out = nxt + ((size_t)ib * (by + 2) + (jb + warp)) * (bz + 2) + kb + lane;
+    unsigned live = 0;  // bit p: cell p of this thread is inside the box
 #pragma unroll
-    for (int h = 0; h < 2; ++h) kok[h] = kb + lane + 32 * h < k1;
-    double worst = 0.0;
+    for (int p = 0; p < PTS; ++p) {
+        const int r = warp + (p >> 1) * NWARP, kk = lane + 32 * (p & 1);
+        if (jb + r < j1 && kb + kk < k1) live |= 1u << p;
+    }
 
-    hx::mbar_wait(&bar[0], 0);
-    hx::mbar_wait(&bar[1 % NSTAGE], 0);
-    for (int q = 1; q <= nplanes - 2; ++q) {
-        const int sm = (q - 1) % NSTAGE, s0 = q % NSTAGE, sp = (q + 1) % NSTAGE;
-        hx::mbar_wait(&bar[sp], ((q + 1) / NSTAGE) & 1);
-        const double *pm = reinterpret_cast<const double *>(smem + sm * STAGE_STRIDE);
-        const double *p0 = reinterpret_cast<const double *>(smem + s0 * STAGE_STRIDE);
-        const double *pp = reinterpret_cast<const double *>(smem + sp * STAGE_STRIDE);
-        const int i = ib - 1 + q;
+    double xm[PTS], x0[PTS];
+    double worst = 0.0;
+    {
+        const double *s0 = reinterpret_cast<const double *>(smem);
+        const double *s1 = reinterpret_cast<const double *>(smem + STAGE_STRIDE);
+        hx::mbar_wait(&bar[0], 0);
+        hx::mbar_wait(&bar[1], 0);
 #pragma unroll
-        for (int rr = 0; rr < ROWS_PER_WARP; ++rr) {
-            const int r = warp + rr * (THREADS / 32);
-            const int j = jb + r;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const int kk = lane + 32 * h;
-                const int ctr = (r + 1) * BOX_Z + kk + 1;
-                const double v = relax(pm[ctr], pp[ctr], p0[ctr - BOX_Z], p0[ctr + BOX_Z],
-                                       p0[ctr - 1], p0[ctr + 1]);
-                if (j < j1 && kok[h]) {
-                    nxt[g.at(i, j, kb + kk)] = v;
-                    if (res) worst = fmax(worst, fabs(__dsub_rn(v, p0[ctr])));
-                }
-            }
-        }
-        __syncthreads();  // every thread is done with stage sm
-        if (threadIdx.x == 0) {
-            const int p = q - 1 + NSTAGE;
-            if (p < nplanes) {
-                hx::mbar_expect_tx(&bar[sm], STAGE_BYTES);
-                hx::tma_load_3d(smem + sm * STAGE_STRIDE, &map, kb - 1, jb - 1, ib - 1 + p, &bar[sm]);
-            }
+        for (int p = 0; p < PTS; ++p) {
+            const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
+            xm[p] = s0[o];
+            x0[p] = s1[o];
         }
     }
-    if (res) cta_max_to_global(worst, res);
+    __syncthreads();  // plane 0 lives in registers now: recycle its stage
+    if (threadIdx.x == 0 && NSTAGE < nplanes) {
+        hx::mbar_expect_tx(&bar[0], STAGE_BYTES);
+        hx::tma_load_3d(smem, &map, kload, jb - 1, ib - 1 + NSTAGE, &bar[0]);
+    }
+    int s_c = 1 % NSTAGE;  // stage holding plane q
+    for (int q = 1; q <= nplanes - 2; ++q) {
+        const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;  // stage holding plane q+1
+        hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
+        const double *P0 = reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE);
+        const double *PP = reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE);
+        double v[PTS];
+        bool fast = true;
+#pragma unroll
+        for (int p = 0; p < PTS; ++p) {
+            const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
+            const double xp = PP[o];
+            v[p] = sum6(xm[p], xp, P0[o - BOX_Z], P0[o + BOX_Z], P0[o - 1], P0[o + 1]);
+            xm[p] = x0[p];
+            x0[p] = xp;
+            fast &= div6_fast_ok(v[p]);
+        }
+        if (fast) {
+#pragma unroll
+            for (int p = 0; p < PTS; ++p) v[p] = div6_fast(v[p]);
+        } else {
+#pragma unroll
+            for (int p = 0; p < PTS; ++p) v[p] = div6(v[p]);
+        }
+#pragma unroll
+        for (int p = 0; p < PTS; ++p) {
+            if (live & (1u << p)) {
+                out[(size_t)((p >> 1) * NWARP) * (bz + 2) + 32 * (p & 1)] = v[p];
+                if (RES) worst = fmax(worst, fabs(__dsub_rn(v[p], xm[p])));
+            }
+        }
+        out += plane;
+        __syncthreads();  // all warps are done with stage s_c (plane q)
+        if (threadIdx.x == 0) {
+            const int p = q + NSTAGE;
+            if (p < nplanes) {
+                hx::mbar_expect_tx(&bar[s_c], STAGE_BYTES);
+                hx::tma_load_3d(smem + s_c * STAGE_STRIDE, &map, kload, jb - 1, ib - 1 + p,
+                                &bar[s_c]);
+            }
+        }
+        s_c = s_n;
+    }
+    if (RES) cta_max_to_global(worst, res);
 }
 
 // ----------------------------------------------------------- generic ----
@@ -165,12 +246,25 @@ stencil_generic_kernel(const double *__restrict__ cur, double *__restrict__ nxt,
     if (k < k1 && j < j1) {
         const size_t c = g.at(i, j, k);
         const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
-        const double v = relax(__ldg(cur + c - sx), __ldg(cur + c + sx), __ldg(cur + c - sy),
-                               __ldg(cur + c + sy), __ldg(cur + c - 1), __ldg(cur + c + 1));
+        const double v = div6(sum6(__ldg(cur + c - sx), __ldg(cur + c + sx), __ldg(cur + c - sy),
+                                   __ldg(cur + c + sy), __ldg(cur + c - 1), __ldg(cur + c + 1)));
         nxt[c] = v;
         if (res) worst = fabs(__dsub_rn(v, __ldg(cur + c)));
     }
     if (res) cta_max_to_global(worst, res);
+}
+
+// Device self-check of div6 against the library division.
+__global__ void div6_check_kernel(const double *in, size_t n, unsigned long long *mismatch) {
+    unsigned long long bad = 0;
+    for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
+         q += (size_t)gridDim.x * blockDim.x) {
+        const double t = in[q];
+        const double a = div6(t), b = __ddiv_rn(t, 6.0);
+        const bool same = (__double_as_longlong(a) == __double_as_longlong(b)) || (a != a && b != b);
+        bad += !same;
+    }
+    if (bad) atomicAdd(mismatch, bad);
 }
 
 // ------------------------------------------------------------- init ------
@@ -199,10 +293,20 @@ __global__ void fill_kernel(double *p, size_t n, double v) {
 
 // ------------------------------------------------------ host helpers -----
 std::mutex g_map_mu;
-std::map<std::tuple<const void *, int, int, int>, CUtensorMap> g_maps;
+std::map<std::tuple<const void *, int, int, int, int, int>, CUtensorMap> g_maps;
 
-int tensor_map_for(const double *cur, int bx, int by, int bz, CUtensorMap *out) {
-    auto key = std::make_tuple((const void *)cur, bx, by, bz);
+int l2_promotion() {
+    if (g_l2promo < 0) {
+        const char *e = getenv("HX_TMA_L2PROMO");  // 0 none, 1 64B, 2 128B, 3 256B
+        g_l2promo = e ? atoi(e) : 1;
+        if (g_l2promo < 0 || g_l2promo > 3) g_l2promo = 1;
+    }
+    return g_l2promo;
+}
+
+int tensor_map_for(const double *cur, int bx, int by, int bz, int box_z, CUtensorMap *out) {
+    const int promo = l2_promotion();
+    auto key = std::make_tuple((const void *)cur, bx, by, bz, box_z, promo);
     {
         std::lock_guard<std::mutex> lk(g_map_mu);
         auto it = g_maps.find(key);
@@ -216,12 +320,12 @@ int tensor_map_for(const double *cur, int bx, int by, int bz, CUtensorMap *out) 
     const cuuint64_t pz = (cuuint64_t)bz + 2, py = (cuuint64_t)by + 2, px = (cuuint64_t)bx + 2;
     cuuint64_t dims[3] = {pz, py, px};
     cuuint64_t strides[2] = {pz * sizeof(double), py * pz * sizeof(double)};
-    cuuint32_t box[3] = {BOX_Z, BOX_Y, 1};
+    cuuint32_t box[3] = {(cuuint32_t)box_z, BOX_Y, 1};
     cuuint32_t estr[3] = {1, 1, 1};
     CUtensorMap m;
     CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)cur, dims, strides, box,
                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        (CUtensorMapL2promotion)promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return HX_E_TMA;
     std::lock_guard<std::mutex> lk(g_map_mu);
     if (g_maps.size() > 256) g_maps.clear();
@@ -244,35 +348,60 @@ int num_sms() {
     return g_num_sms;
 }
 
-int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
-               int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
-    CUtensorMap map;
-    int rc = tensor_map_for(cur, bx, by, bz, &map);
-    if (rc) return rc;
+template <bool RES, int BOX_Z>
+int launch_tma_t(const CUtensorMap &map, double *nxt, int by, int bz, int i0, int i1, int j0,
+                 int j1, int k0, int k1, int ntj, int ntk, int chunk, int nchunks, int grows, long items,
+                 unsigned long long *res, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        HX_TRY(cudaFuncSetAttribute(stencil_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)SMEM_BYTES));
+        HX_TRY(cudaFuncSetAttribute(stencil_tma_kernel<RES, BOX_Z>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
         attr_set = true;
     }
+    stencil_tma_kernel<RES, BOX_Z><<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
+        map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk, chunk, nchunks, grows, res);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
+int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
+               int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
+    // every tile starts at kb = k0 + t*TZ (TZ even): one box width per launch
+    const bool shifted = ((k0 - 1) & 1) != 0;
+    const int box_z = shifted ? TZ + 4 : TZ + 2;
+    CUtensorMap map;
+    int rc = tensor_map_for(cur, bx, by, bz, box_z, &map);
+    if (rc) return rc;
     const int ni = i1 - i0, nj = j1 - j0, nk = k1 - k0;
     const int ntj = (nj + TY - 1) / TY, ntk = (nk + TZ - 1) / TZ;
     int chunk = g_chunk;
     if (chunk <= 0) {
-        // ~24 waves of 2 CTAs/SM keeps the tail short; chunk-boundary planes
-        // are re-read once per chunk (2/chunk extra read traffic).
-        const long target = 24L * 2 * num_sms();
-        const long tiles = (long)ntj * ntk;
-        chunk = (int)std::max<long>(8, ((long)ni * tiles + target - 1) / target);
+        // Short chunks keep neighbouring CTAs in step (their tile halos are
+        // L2 hits); the grouped order below makes the 2 boundary planes a
+        // chunk shares with the next one L2 hits too.
+        // Tuned on B200 at 1536^3 (tools/prof_stencil.py sweeps, profiles/):
+        // chunk 4 with ~288-tile groups reaches ~99% of the measured copy
+        // bandwidth; chunk 10 / ungrouped was 87%, chunk 96 70%.
+        const char *e = getenv("HX_STENCIL_CHUNK");
+        chunk = e ? atoi(e) : 4;
+        if (chunk <= 0) chunk = 4;
     }
     chunk = std::min(chunk, ni);
     const int nchunks = (ni + chunk - 1) / chunk;
+    int grows = std::max(1, (288 + ntk / 2) / ntk);  // tile rows per scheduling group
+    if (const char *e = getenv("HX_STENCIL_GROUP")) grows = std::max(1, atoi(e));
+    grows = std::min(grows, ntj);
     const long items = (long)ntj * ntk * nchunks;
     if (items > 0x7fffffffL) return HX_E_INVALID;
-    stencil_tma_kernel<<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
-        map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk, chunk, res);
-    HX_LAUNCH_CHECK();
-    return 0;
+    if (shifted)
+        return res ? launch_tma_t<true, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
+                                                chunk, nchunks, grows, items, res, st)
+                   : launch_tma_t<false, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
+                                                 chunk, nchunks, grows, items, res, st);
+    return res ? launch_tma_t<true, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
+                                            chunk, nchunks, grows, items, res, st)
+               : launch_tma_t<false, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
+                                             chunk, nchunks, grows, items, res, st);
 }
 
 int launch_generic(const double *cur, double *nxt, int by, int bz, int i0, int i1, int j0, int j1,
@@ -327,6 +456,14 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
 int hx_stencil(const double *cur, double *nxt, int bx, int by, int bz, unsigned long long *res,
                void *stream) {
     return hx_stencil_box(cur, nxt, bx, by, bz, 1, bx + 1, 1, by + 1, 1, bz + 1, res, stream);
+}
+
+int hx_div6_check(const double *in, size_t n, unsigned long long *mismatches, void *stream) {
+    if (!in || !mismatches) return HX_E_INVALID;
+    if (!n) return 0;
+    div6_check_kernel<<<4 * num_sms(), 256, 0, (cudaStream_t)stream>>>(in, n, mismatches);
+    HX_LAUNCH_CHECK();
+    return 0;
 }
 
 int hx_init_block(double *field, int bx, int by, int bz, int hot_wall, double hot,

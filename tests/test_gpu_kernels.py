@@ -75,6 +75,28 @@ def test_stencil_bitexact_vs_oracle(hx, shape, variant):
         assert hx.raw("hx_stencil_last_variant")() == 1  # the TMA pipeline ran
 
 
+def test_div6_matches_correctly_rounded_division(hx):
+    """The stencil's division (RN(1/6) product + one FMA correction) equals
+    the library's correctly rounded division on 2^27 random bit patterns
+    per exponent band, plus zeros, subnormals, extremes and non-finites."""
+    g = torch.Generator(device="cuda").manual_seed(1234)
+    bad = torch.zeros(1, dtype=torch.int64, device="cuda")
+    n = 1 << 27
+    for lo, hi in ((0x3C0, 0x440), (0x000, 0x7FF), (0x3FE, 0x402)):
+        bits = torch.randint(0, 1 << 52, (n,), generator=g, device="cuda", dtype=torch.int64)
+        exp = torch.randint(lo, hi, (n,), generator=g, device="cuda", dtype=torch.int64)
+        sign = torch.randint(0, 2, (n,), generator=g, device="cuda", dtype=torch.int64)
+        x = (bits | (exp << 52) | (sign << 63)).view(torch.float64)
+        hx.call("hx_div6_check", x.data_ptr(), n, bad.data_ptr(), stream())
+    special = torch.tensor([0.0, -0.0, 5e-324, -5e-324, 2.2250738585072014e-308, 1.7976931348623157e308,
+                            -1.7976931348623157e308, float("inf"), float("-inf"), float("nan"), 6.0,
+                            3.0, 1.0] + [float.fromhex(h) for h in (
+                            "0x1p-960", "0x1p1020", "0x1.fffffffffffffp-961", "0x1.0000000000001p1020")], dtype=torch.float64, device="cuda")
+    hx.call("hx_div6_check", special.data_ptr(), special.numel(), bad.data_ptr(), stream())
+    torch.cuda.synchronize()
+    assert int(bad.item()) == 0
+
+
 def test_tma_forced_on_even_z(hx):
     rng = np.random.default_rng(5)
     cur = rng.standard_normal((40, 36, 66))
