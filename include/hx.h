@@ -78,6 +78,8 @@ int hx_ipc_close(void *base);
 int hx_memcpy(void *dst, const void *src, size_t bytes, void *stream);          /* cudaMemcpyDefault */
 int hx_memcpy_peer(void *dst, int dst_dev, const void *src, int src_dev, size_t bytes, void *stream);
 int hx_copy_sm(void *dst, const void *src, size_t bytes, void *stream);         /* SM-issued (peer ok) */
+/* count back-to-back copies src -> dst in one launch (OSU window). */
+int hx_copy_sm_window(void *dst, const void *src, size_t bytes, int count, void *stream);
 int hx_fill_f64(double *dst, size_t n, double value, void *stream);
 
 /* ------------------------------------------------------------- stencil ---
@@ -160,6 +162,16 @@ int hx_pingpong(int role, const void *src, void *peer_dst, size_t bytes,
                 unsigned long long *my_flag, unsigned long long *peer_flag,
                 int iters, int warmup, unsigned long long timeout_ns,
                 unsigned long long *elapsed_ns, int *err, void *stream);
+
+/* Low-latency variant for small messages (bytes % 4 == 0, <= 1 MiB): each
+ * 8-byte word of the LL buffers carries 4 payload bytes plus the 32-bit
+ * iteration tag and is written with one single-copy-atomic store, so the
+ * receiver polls the data itself (no fence, no separate flag). peer_ll /
+ * my_ll: 2*bytes each (my_ll zeroed by the caller); dst_local: bytes. One
+ * CTA per GPU; both roles must run concurrently on different GPUs. */
+int hx_pingpong_ll(int role, const void *src, void *dst_local, void *peer_ll, void *my_ll,
+                   size_t bytes, int iters, int warmup, unsigned long long timeout_ns,
+                   unsigned long long *elapsed_ns, int *err, void *stream);
 
 #ifdef __cplusplus
 }

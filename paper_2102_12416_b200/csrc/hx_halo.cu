@@ -16,6 +16,8 @@
 // receiver acquires it before reading the slot.
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "hx_internal.cuh"
 
 namespace cg = cooperative_groups;
@@ -56,6 +58,28 @@ __device__ __forceinline__ void copy_segment(const FaceJob &J, int row, int c0, 
     const hx::Face &f = J.f;
     const size_t frow = (size_t)f.base + (size_t)row * f.row_stride;
     const size_t crow = (size_t)row * f.cols;
+    // The face (slot) side is contiguous: move it as 16-byte pairs when its
+    // segment start is 16-byte aligned (NVLink sees half as many stores).
+    const double *cside = PACK ? J.dst + crow + c0 : J.src + crow + c0;
+    if ((((uintptr_t)cside) & 15) == 0) {
+        const int npair = (c1 - c0) >> 1;
+        for (int p = threadIdx.x; p < npair; p += blockDim.x) {
+            const int c = c0 + 2 * p;
+            const size_t fa = frow + (size_t)c * f.col_stride, fb = fa + f.col_stride;
+            if (PACK) {
+                double2 v;
+                v.x = LD_CG ? __ldcg(J.src + fa) : J.src[fa];
+                v.y = LD_CG ? __ldcg(J.src + fb) : J.src[fb];
+                *reinterpret_cast<double2 *>(J.dst + crow + c) = v;
+            } else {
+                const double2 *s = reinterpret_cast<const double2 *>(J.src + crow + c);
+                const double2 v = LD_CG ? __ldcg(s) : *s;
+                J.dst[fa] = v.x;
+                J.dst[fb] = v.y;
+            }
+        }
+        c0 += 2 * npair;  // odd tail (at most one element)
+    }
     for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
         const size_t fi = frow + (size_t)c * f.col_stride;
         if (PACK) {
@@ -87,9 +111,12 @@ pack_put_kernel(FaceBatch b, unsigned long long value, unsigned int *counters) {
     const int c0 = (local % J.col_blocks) * FACE_COLS_PER_BLOCK;
     copy_segment<true, false>(J, row, c0, min(c0 + FACE_COLS_PER_BLOCK, J.f.cols));
     if (J.flag == nullptr) return;
-    __threadfence_system();  // this thread's peer stores are visible system-wide
+    // The CTA barrier orders every thread's peer stores before thread 0's
+    // system-scope fence (fences are cumulative), which precedes the counter
+    // atomic; the last CTA fences again and release-stores the flag.
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence_system();
         const unsigned nblk = (unsigned)(J.f.rows * J.col_blocks);
         const unsigned done = atomicAdd(&counters[q], 1u) + 1u;
         if (done == nblk) {
@@ -125,23 +152,108 @@ __global__ void wait_flag_kernel(const unsigned long long *flag, unsigned long l
     hx::spin_until(flag, value, timeout_ns, err);
 }
 
-// Grid-stride byte copy, 16-byte vectors when both ends are aligned.
+// Grid-stride byte copy: 16-byte vectors (4 in flight per thread) when both
+// ends are aligned, byte tail otherwise.
 __device__ __forceinline__ void copy_bytes(char *dst, const char *src, size_t n, size_t tid,
                                            size_t nthreads, bool ld_cg) {
     if ((((uintptr_t)dst | (uintptr_t)src) & 15) == 0) {
         const size_t nv = n / 16;
         uint4 *d = reinterpret_cast<uint4 *>(dst);
         const uint4 *s = reinterpret_cast<const uint4 *>(src);
-        for (size_t q = tid; q < nv; q += nthreads) d[q] = ld_cg ? __ldcg(s + q) : s[q];
-        for (size_t q = nv * 16 + tid; q < n; q += nthreads) dst[q] = src[q];
+        size_t q = tid;
+        for (; q + 3 * nthreads < nv; q += 4 * nthreads) {
+            uint4 a, b, c, e;
+            if (ld_cg) {
+                a = __ldcg(s + q); b = __ldcg(s + q + nthreads);
+                c = __ldcg(s + q + 2 * nthreads); e = __ldcg(s + q + 3 * nthreads);
+            } else {
+                a = s[q]; b = s[q + nthreads]; c = s[q + 2 * nthreads]; e = s[q + 3 * nthreads];
+            }
+            d[q] = a; d[q + nthreads] = b; d[q + 2 * nthreads] = c; d[q + 3 * nthreads] = e;
+        }
+        for (; q < nv; q += nthreads) d[q] = ld_cg ? __ldcg(s + q) : s[q];
+        for (size_t b = nv * 16 + tid; b < n; b += nthreads) dst[b] = src[b];
     } else {
         for (size_t q = tid; q < n; q += nthreads) dst[q] = src[q];
     }
 }
 
-__global__ void copy_kernel(char *dst, const char *src, size_t n) {
+__global__ void __launch_bounds__(256) copy_kernel(char *dst, const char *src, size_t n) {
     copy_bytes(dst, src, n, blockIdx.x * (size_t)blockDim.x + threadIdx.x,
                (size_t)gridDim.x * blockDim.x, false);
+}
+
+// A window of `count` back-to-back messages src -> dst in ONE launch (the
+// OSU bandwidth window without per-message kernel boundaries).
+__global__ void __launch_bounds__(256) copy_window_kernel(char *dst, const char *src, size_t n,
+                                                          int count) {
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t nth = (size_t)gridDim.x * blockDim.x;
+    // loads bypass L1 (ld.cg): a pulled source must cross NVLink every time
+    for (int m = 0; m < count; ++m) copy_bytes(dst, src, n, tid, nth, true);
+}
+
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Low-latency (LL) ping-pong: every 8-byte word carries 4 payload bytes and
+// the 32-bit iteration tag, written with one single-copy-atomic store, so
+// the receiver polls the data itself — no fence, no separate flag.
+__device__ __forceinline__ bool ll_recv(const unsigned long long *ll, unsigned *out, int nwords,
+                                        unsigned tag, unsigned long long t0,
+                                        unsigned long long timeout_ns, int *err) {
+    for (int w = threadIdx.x; w < nwords; w += blockDim.x) {
+        unsigned long long v;
+        unsigned polls = 0;
+        while (((v = ld_relaxed_sys(ll + w)) >> 32) != tag) {
+            if ((++polls & 255) == 0 && hx::globaltimer() - t0 > timeout_ns) {
+                atomicExch(err, HX_E_TIMEOUT);
+                return false;
+            }
+        }
+        out[w] = (unsigned)v;
+    }
+    return true;
+}
+
+__global__ void pingpong_ll_kernel(int role, const unsigned *src, unsigned *dst_local,
+                                   unsigned long long *peer_ll, const unsigned long long *my_ll,
+                                   int nwords, int iters, int warmup, unsigned long long timeout_ns,
+                                   unsigned long long *elapsed, int *err) {
+    __shared__ int ok;
+    const unsigned long long start = hx::globaltimer();
+    unsigned long long t0 = start;
+    for (int it = 0; it < warmup + iters; ++it) {
+        const unsigned tag = (unsigned)it + 1;
+        if (role == 0 && it == warmup && threadIdx.x == 0) t0 = hx::globaltimer();
+        if (role == 1) {
+            const bool good = ll_recv(my_ll, dst_local, nwords, tag, start, timeout_ns, err);
+            if (threadIdx.x == 0) ok = 1;
+            __syncthreads();
+            if (!good) ok = 0;
+            __syncthreads();
+            if (!ok) return;
+        }
+        const unsigned *out = role == 0 ? src : dst_local;
+        for (int w = threadIdx.x; w < nwords; w += blockDim.x)
+            st_relaxed_sys(peer_ll + w, ((unsigned long long)tag << 32) | out[w]);
+        if (role == 0) {
+            const bool good = ll_recv(my_ll, dst_local, nwords, tag, start, timeout_ns, err);
+            if (threadIdx.x == 0) ok = 1;
+            __syncthreads();
+            if (!good) ok = 0;
+            __syncthreads();
+            if (!ok) return;
+        }
+    }
+    if (role == 0 && threadIdx.x == 0 && elapsed) *elapsed = hx::globaltimer() - t0;
 }
 
 // Device-level OSU ping-pong: cooperative grid so every CTA is resident.
@@ -159,16 +271,18 @@ __global__ void pingpong_kernel(int role, const char *src, char *peer_dst, size_
         const unsigned long long v = (unsigned long long)it + 1;
         if (role == 0 && it == warmup && lead) t0 = hx::globaltimer();
         if (role == 1) {
-            if (threadIdx.x == 0) ok = hx::spin_until(my_flag, v, timeout_ns, err);
+            if (threadIdx.x == 0) ok = hx::spin_until(my_flag, v, timeout_ns, err, 0);
             __syncthreads();
             if (!ok) return;
         }
         copy_bytes(peer_dst, src, bytes, tid, nthr, role == 1);
-        __threadfence_system();
-        grid.sync();
-        if (lead) hx::st_release_sys(peer_flag, v);
+        // barrier(s) order every thread's peer stores before the lead's
+        // system-scope fence (cumulative) and the release of the flag
+        __syncthreads();
+        if (gridDim.x > 1) grid.sync();
+        if (lead) hx::st_release_sys(peer_flag, v);  // release = MEMBAR.SYS + strong store
         if (role == 0) {
-            if (threadIdx.x == 0) ok = hx::spin_until(my_flag, v, timeout_ns, err);
+            if (threadIdx.x == 0) ok = hx::spin_until(my_flag, v, timeout_ns, err, 0);
             __syncthreads();
             if (!ok) return;
         }
@@ -276,6 +390,22 @@ int hx_wait_flag(unsigned long long *flag, unsigned long long value, unsigned lo
     return 0;
 }
 
+int hx_pingpong_ll(int role, const void *src, void *dst_local, void *peer_ll, void *my_ll,
+                   size_t bytes, int iters, int warmup, unsigned long long timeout_ns,
+                   unsigned long long *elapsed_ns, int *err, void *stream) {
+    if ((role != 0 && role != 1) || !dst_local || !peer_ll || !my_ll || !err || iters < 0 ||
+        warmup < 0 || bytes == 0 || (bytes & 3) || bytes > (1u << 20))
+        return HX_E_INVALID;
+    if (role == 0 && !src) return HX_E_INVALID;
+    const int nwords = (int)(bytes / 4);
+    const int threads = nwords >= 1024 ? 1024 : ((nwords + 31) / 32) * 32;
+    pingpong_ll_kernel<<<1, threads, 0, (cudaStream_t)stream>>>(
+        role, (const unsigned *)src, (unsigned *)dst_local, (unsigned long long *)peer_ll,
+        (const unsigned long long *)my_ll, nwords, iters, warmup, timeout_ns, elapsed_ns, err);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
 int hx_copy_sm(void *dst, const void *src, size_t bytes, void *stream) {
     if (!bytes) return 0;
     if (!dst || !src) return HX_E_INVALID;
@@ -285,6 +415,26 @@ int hx_copy_sm(void *dst, const void *src, size_t bytes, void *stream) {
     size_t want = (bytes / 16 + 255) / 256;
     unsigned grid = (unsigned)(want < (size_t)sms * 4 ? (want ? want : 1) : (size_t)sms * 4);
     copy_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((char *)dst, (const char *)src, bytes);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
+int hx_copy_sm_window(void *dst, const void *src, size_t bytes, int count, void *stream) {
+    if (!bytes || count <= 0) return 0;
+    if (!dst || !src) return HX_E_INVALID;
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    static int mult = 0;
+    if (!mult) {
+        const char *e = getenv("HX_COPY_GRID_MULT");
+        mult = e ? atoi(e) : 4;
+        if (mult <= 0) mult = 4;
+    }
+    size_t want = (bytes * (size_t)count / 64 + 255) / 256;  // ~16 KiB of window per CTA
+    unsigned grid = (unsigned)(want < (size_t)sms * mult ? (want ? want : 1) : (size_t)sms * mult);
+    copy_window_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>((char *)dst, (const char *)src,
+                                                               bytes, count);
     HX_LAUNCH_CHECK();
     return 0;
 }

@@ -76,18 +76,23 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 
 // Spin (one thread) until *flag >= value or the deadline passes.
 // Returns true on success; on timeout records HX_E_TIMEOUT in *err.
+// max_sleep_ns bounds the exponential __nanosleep back-off (0 = pure spin,
+// for latency-critical ping-pong; the deadline check is every 64 polls).
 __device__ __forceinline__ bool spin_until(const unsigned long long *flag, unsigned long long value,
-                                           unsigned long long timeout_ns, int *err) {
+                                           unsigned long long timeout_ns, int *err,
+                                           unsigned max_sleep_ns = 256) {
     if (ld_acquire_sys(flag) >= value) return true;
     const unsigned long long t0 = globaltimer();
-    unsigned ns = 32;
+    unsigned ns = 16, polls = 0;
     while (ld_acquire_sys(flag) < value) {
-        if (globaltimer() - t0 > timeout_ns) {
+        if ((++polls & 63) == 0 && globaltimer() - t0 > timeout_ns) {
             if (err) atomicExch(err, HX_E_TIMEOUT);
             return false;
         }
-        __nanosleep(ns);
-        if (ns < 1024) ns <<= 1;
+        if (max_sleep_ns) {
+            __nanosleep(ns);
+            if (ns < max_sleep_ns) ns <<= 1;
+        }
     }
     return true;
 }

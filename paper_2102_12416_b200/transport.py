@@ -199,6 +199,18 @@ class Worker:
         if nbytes <= self.cfg.eager_threshold:
             ready, keep = None, None
             if isinstance(source, DeviceRegion):
+                ready = torch.cuda.Event()
+                ready.record(self.space.stream_of(source.buffer.owner))
+                direct = Frame(FRAME_EAGER, tag, nbytes, source, ready, self.id)
+                if peer._match_now(direct):
+                    # the receive was already posted: one direct HBM/NVLink
+                    # copy, and the sender's stream is ordered behind it, so
+                    # the source is reusable at once (eager semantics)
+                    self.stats["tx_eager"] += 1
+                    self.stats["tx_direct"] += 1
+                    self.stats["sends"] += 1
+                    self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
+                    return
                 source, ready, keep = self._snapshot(source)
             frame = Frame(FRAME_EAGER, tag, nbytes, source, ready, self.id, keepalive=keep)
             self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
@@ -208,9 +220,30 @@ class Worker:
                 ready = torch.cuda.Event()
                 ready.record(self.space.stream_of(source.buffer.owner))
             frame = Frame(FRAME_RTS, tag, nbytes, source, ready, self.id, send_completion=completion)
+            if isinstance(source, DeviceRegion) and peer._match_now(frame):
+                self.stats["tx_rts"] += 1
+                self.stats["tx_direct"] += 1
+                self.stats["sends"] += 1
+                return
         self.stats[f"tx_{_NAMES[frame.kind]}"] += 1
         self.stats["sends"] += 1
         peer.inbound.append(frame)
+
+    def _match_now(self, frame: Frame) -> bool:
+        """Receiver side of a direct send: if a posted receive matches and no
+        earlier frame from the same sender is still queued (FIFO per pair) or
+        parked by a hold predicate, absorb the frame immediately."""
+        if self.hold is not None or any(f.src == frame.src for f in self.inbound):
+            return False
+        for i, req in enumerate(self.posted):
+            if req.matches(frame.tag):
+                del self.posted[i]
+                frame.seq = self._arrival_seq
+                self._arrival_seq += 1
+                self.stats[f"rx_{_NAMES[frame.kind]}"] += 1
+                self._absorb(req, frame)
+                return True
+        return False
 
     def _snapshot(self, src: DeviceRegion):
         """Stream-ordered copy of an eager device payload into a bounce buffer."""
@@ -354,6 +387,11 @@ class Worker:
         if isinstance(sink, DeviceRegion):
             ev = self._d2d(sink, src, n, frame.ready)
             keep = frame.keepalive
+            if (frame.kind == FRAME_EAGER and isinstance(src, DeviceRegion)
+                    and src.buffer.owner != sink.buffer.owner):
+                # direct eager send: later work on the sender's stream must
+                # not overwrite the source before the copy has read it
+                self.space.stream_of(src.buffer.owner).wait_event(ev)
 
             def landed(keep=keep):
                 done()
