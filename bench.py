@@ -196,6 +196,8 @@ def main() -> int:
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--overlap", type=int, default=1,
+                    help="1: interior sweep concurrent with the halo exchange (default)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -219,7 +221,7 @@ def main() -> int:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dims = global_dims(world, args.block)
     eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: local,
-                     dist=dist if world > 1 else None)
+                     dist=dist if world > 1 else None, overlap=bool(args.overlap))
     b = eng.blocks[rank]
     s = eng.stream_of(b)
 
@@ -237,33 +239,34 @@ def main() -> int:
         return float(t.item())
 
     # ---- device-timed steps (inputs resident in HBM)
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    xev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-           for _ in range(args.steps)]
+    timing: dict = {}
     start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         for _ in range(args.warmup):
             eng.step()
         barrier()
         start.record(s)
-        for k in range(args.steps):
-            xev[k][0].record(s)
-            if b.nbr_dirs:
-                eng._put(b, eng.it)
-                eng._wait(b, eng.it)
-            xev[k][1].record(s)
-            ev[k][0].record(s)
-            eng._relax(b, None)
-            ev[k][1].record(s)
-            eng.it += 1
+        for _ in range(args.steps):
+            eng.step(timing=timing)
         stop.record(s)
         barrier()
     eng.check_errors()
+
+    def mean_ms(name):
+        pairs = timing.get(name, [])
+        return statistics.mean(a.elapsed_time(z) for a, z in pairs) if pairs else 0.0
+
     t_ms = max_over_ranks(start.elapsed_time(stop))
-    sten_ms = statistics.mean(a.elapsed_time(z) for a, z in ev)
-    xch_ms = max_over_ranks(statistics.mean(a.elapsed_time(z) for a, z in xev))
-    launches = args.steps * (1 + (2 if b.nbr_dirs else 0)) * world
+    if eng.overlap and b.nbr_dirs:
+        sten_ms = mean_ms("interior") + mean_ms("shell")  # the sweep kernels, not the wait
+        exposed_ms = max_over_ranks(mean_ms("exposed"))
+        launches_per_step = 1 + len(eng.boxes(b)[1]) + 1 + 2 * len(b.nbr_dirs)
+    else:
+        sten_ms = mean_ms("sweep")
+        exposed_ms = max_over_ranks(mean_ms("exchange"))
+        launches_per_step = 1 + (2 if b.nbr_dirs else 0)
+    xch_ms = max_over_ranks(mean_ms("exchange"))
+    launches = args.steps * launches_per_step * world
     cells = b.cells
     total_cells = cells * world
     value = total_cells * args.steps / (t_ms * 1e-3) / 1e9
@@ -298,7 +301,9 @@ def main() -> int:
             "halo": ({"bytes_out_per_rank": face_bytes, "exchange_ms": xch_ms,
                       "exchange_gbs": face_bytes / (xch_ms * 1e-3) / 1e9,
                       "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS,
-                      "non_overlapped_frac": xch_ms / (t_ms / args.steps)} if world > 1 else None),
+                      "overlap": eng.overlap, "exposed_ms": exposed_ms,
+                      "interior_ms": mean_ms("interior"), "shell_ms": mean_ms("shell"),
+                      "non_overlapped_frac": exposed_ms / (t_ms / args.steps)} if world > 1 else None),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -404,6 +404,54 @@ int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, i
                                              chunk, nchunks, grows, items, res, st);
 }
 
+// Thin boundary slabs of the overlap split (one plane / row / column thick):
+// one thread per cell over the flattened box, consecutive threads along the
+// box's longest fast axis (k if the slab spans k, else j) so the centre
+// loads coalesce; neighbours come through L1/L2.
+__global__ void __launch_bounds__(256)
+stencil_slab_kernel(const double *__restrict__ cur, double *__restrict__ nxt, int by, int bz,
+                    int i0, int j0, int k0, int ni, int nj, int nk, int k_fast,
+                    unsigned long long *res) {
+    const hx::Geom g(by, bz);
+    const long long n = (long long)ni * nj * nk;
+    double worst = 0.0;
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        int i, j, k;
+        if (k_fast) {
+            k = k0 + (int)(q % nk);
+            const long long r = q / nk;
+            j = j0 + (int)(r % nj);
+            i = i0 + (int)(r / nj);
+        } else {
+            j = j0 + (int)(q % nj);
+            const long long r = q / nj;
+            k = k0 + (int)(r % nk);
+            i = i0 + (int)(r / nk);
+        }
+        const size_t c = g.at(i, j, k);
+        const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
+        const double v = div6(sum6(__ldg(cur + c - sx), __ldg(cur + c + sx), __ldg(cur + c - sy),
+                                   __ldg(cur + c + sy), __ldg(cur + c - 1), __ldg(cur + c + 1)));
+        nxt[c] = v;
+        if (res) worst = fmax(worst, fabs(__dsub_rn(v, __ldg(cur + c))));
+    }
+    if (res) cta_max_to_global(worst, res);
+}
+
+int launch_slab(const double *cur, double *nxt, int by, int bz, int i0, int i1, int j0, int j1,
+                int k0, int k1, unsigned long long *res, cudaStream_t st) {
+    const int ni = i1 - i0, nj = j1 - j0, nk = k1 - k0;
+    const long long n = (long long)ni * nj * nk;
+    const int k_fast = (nk >= 32 || nk >= nj) ? 1 : 0;
+    const long long want = (n + 255) / 256;
+    const unsigned grid = (unsigned)std::min<long long>(want, 16LL * num_sms());
+    stencil_slab_kernel<<<grid, 256, 0, st>>>(cur, nxt, by, bz, i0, j0, k0, ni, nj, nk, k_fast,
+                                              res);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
 int launch_generic(const double *cur, double *nxt, int by, int bz, int i0, int i1, int j0, int j1,
                    int k0, int k1, unsigned long long *res, cudaStream_t st) {
     dim3 blk(32, 8, 1);
@@ -439,7 +487,16 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
     if (i0 >= i1 || j0 >= j1 || k0 >= k1) return 0;  // empty box
     cudaStream_t st = (cudaStream_t)stream;
     int want = g_variant;
-    if (want == 0) want = tma_eligible(cur, bz) ? 1 : 2;
+    if (want == 0) {
+        // thin slabs (the overlap split's boundary shell) would waste most of
+        // a 32x64 TMA tile; they get the flattened slab kernel
+        const bool thin = (j1 - j0) < 8 || (k1 - k0) < 16;
+        want = thin ? 3 : (tma_eligible(cur, bz) ? 1 : 2);
+    }
+    if (want == 3) {
+        g_last_variant = 3;
+        return launch_slab(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);
+    }
     if (want == 1 && !tma_eligible(cur, bz)) return HX_E_INVALID;
     if (want == 1) {
         int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);

@@ -117,6 +117,26 @@ class HaloBlock:
         return self.bx * self.by * self.bz
 
 
+class _Marks:
+    """CUDA event pairs per (name, block) for optional step timing."""
+
+    def __init__(self, timing):
+        self.t = timing
+        self.open = {}
+
+    def begin(self, name, b, stream):
+        if self.t is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            self.open[(name, b.rank)] = e
+
+    def end(self, name, b, stream):
+        if self.t is not None:
+            e = torch.cuda.Event(enable_timing=True)
+            e.record(stream)
+            self.t.setdefault(name, []).append((self.open.pop((name, b.rank)), e))
+
+
 def exchange_table(dist, mine):
     """All-gather each process's (rank, ipc handle, offset, device) arena
     records — the one-time persistent-channel set-up. Without a process
@@ -139,8 +159,9 @@ class HaloJacobi:
     """
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
-                 policy: str = "reference", timeout_s: float = 30.0):
+                 policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False):
         self.dims = tuple(dims)
+        self.overlap = overlap
         self.pes = pes
         self.grid = (decompose if policy == "reference" else decompose_b200)(self.dims, pes)
         self.local_ranks = list(range(pes)) if local_ranks is None else list(local_ranks)
@@ -150,9 +171,13 @@ class HaloJacobi:
         self.timeout_ns = int(timeout_s * 1e9)
         self.blocks = {r: HaloBlock(self.dims, self.grid, r, self.device_of(r)) for r in self.local_ranks}
         self.streams = {}
+        self.comm = {}
         for b in self.blocks.values():
             if b.device not in self.streams:
                 self.streams[b.device] = torch.cuda.Stream(device=b.device)
+                # halo traffic on a high-priority stream so its few CTAs are
+                # scheduled ahead of the queued interior-sweep CTAs
+                self.comm[b.device] = torch.cuda.Stream(device=b.device, priority=-1)
         self.it = 0
         self._ipc_bases = []
         self._res = {}
@@ -231,28 +256,134 @@ class HaloJacobi:
                   self.stream_of(b).cuda_stream)
         b.cur ^= 1
 
-    def step(self, residual: bool = False) -> None:
-        """One iteration on every local block (enqueue only, no host sync)."""
+    def _res_ptr(self, b: HaloBlock, it: int, residual: bool):
+        if not residual:
+            return None
+        buf = self._res.setdefault(b.rank, [])
+        if len(buf) <= it:
+            buf.append(torch.zeros(1, dtype=torch.int64, device=f"cuda:{b.device}"))
+        return buf[it].data_ptr()
+
+    def step(self, residual: bool = False, timing: dict | None = None) -> None:
+        """One iteration on every local block (enqueue only, no host sync).
+
+        timing (optional): dict of lists receiving CUDA event pairs per block
+        — 'exchange' (put + wait + unpack), 'sweep' (all stencil work), and in
+        overlap mode 'interior', 'exposed' (main stream stalled on the halo)
+        and 'shell'."""
+        if self.overlap:
+            return self._step_overlap(residual, timing)
         it = self.it
         blocks = list(self.blocks.values())
+        mark = _Marks(timing)
         for b in blocks:
             if b.nbr_dirs:
                 _lib.call("hx_set_device", b.device)
+                mark.begin("exchange", b, self.stream_of(b))
                 self._put(b, it)
         for b in blocks:
             if b.nbr_dirs:
                 _lib.call("hx_set_device", b.device)
                 self._wait(b, it)
+                mark.end("exchange", b, self.stream_of(b))
         for b in blocks:
             _lib.call("hx_set_device", b.device)
-            res_ptr = None
-            if residual:
-                buf = self._res.setdefault(b.rank, [])
-                if len(buf) <= it:
-                    t = torch.zeros(1, dtype=torch.int64, device=f"cuda:{b.device}")
-                    buf.append(t)
-                res_ptr = buf[it].data_ptr()
-            self._relax(b, res_ptr)
+            mark.begin("sweep", b, self.stream_of(b))
+            self._relax(b, self._res_ptr(b, it, residual))
+            mark.end("sweep", b, self.stream_of(b))
+        self.it += 1
+
+    # ------------------------------------------------------- overlap mode --
+
+    def boxes(self, b: HaloBlock):
+        """Interior box (cells that read no neighbour-fed ghost) and the
+        disjoint boundary slabs toward neighbours, 1-based [lo, hi) triples."""
+        n = (b.bx, b.by, b.bz)
+        nb = b.neighbors
+        lo = [2 if nb[2 * a] is not None else 1 for a in range(3)]
+        hi = [n[a] if nb[2 * a + 1] is not None else n[a] + 1 for a in range(3)]
+        inner = (lo[0], hi[0], lo[1], hi[1], lo[2], hi[2])
+        shells = []
+        if nb[0] is not None:
+            shells.append((1, 2, 1, b.by + 1, 1, b.bz + 1))
+        if nb[1] is not None:
+            shells.append((b.bx, b.bx + 1, 1, b.by + 1, 1, b.bz + 1))
+        if nb[2] is not None:
+            shells.append((lo[0], hi[0], 1, 2, 1, b.bz + 1))
+        if nb[3] is not None:
+            shells.append((lo[0], hi[0], b.by, b.by + 1, 1, b.bz + 1))
+        if nb[4] is not None:
+            shells.append((lo[0], hi[0], lo[1], hi[1], 1, 2))
+        if nb[5] is not None:
+            shells.append((lo[0], hi[0], lo[1], hi[1], b.bz, b.bz + 1))
+        return inner, [x for x in shells if x[0] < x[1] and x[2] < x[3] and x[4] < x[5]]
+
+    def _box(self, b: HaloBlock, box, res_ptr, stream) -> None:
+        if box[0] < box[1] and box[2] < box[3] and box[4] < box[5]:
+            _lib.call("hx_stencil_box", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz,
+                      *box, res_ptr, stream.cuda_stream)
+
+    def _step_overlap(self, residual: bool, timing) -> None:
+        """Interior sweep concurrent with the halo exchange (paper §4.3's
+        overlap): comm stream = put, wait, unpack; main stream = interior
+        box, then (after the halo event) the boundary slabs."""
+        it, p = self.it, self.it & 1
+        blocks = list(self.blocks.values())
+        mark = _Marks(timing)
+        halo_done = {}
+        for b in blocks:  # phase 1: puts (comm stream, after the last sweep)
+            if not b.nbr_dirs:
+                continue
+            _lib.call("hx_set_device", b.device)
+            s, c = self.stream_of(b), self.comm[b.device]
+            ready = torch.cuda.Event()
+            ready.record(s)
+            c.wait_event(ready)
+            mark.begin("exchange", b, c)
+            dst = [b.put_slot(d, p) if d in b.nbr_dirs else None for d in range(NDIRS)]
+            flg = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+            _lib.call("hx_pack_put", b.field_ptr(), b.bx, b.by, b.bz, b.dir_mask,
+                      _lib.ptr_array(dst), _lib.ptr_array(flg), it + 1, b.counters_ptr,
+                      c.cuda_stream)
+        for b in blocks:  # phase 2: one-thread flag waits, then unpacks (comm stream)
+            if not b.nbr_dirs:
+                continue
+            _lib.call("hx_set_device", b.device)
+            c = self.comm[b.device]
+            for d in b.nbr_dirs:
+                _lib.call("hx_wait_flag", b.flag_ptr(d), it + 1, self.timeout_ns, b.err_ptr,
+                          c.cuda_stream)
+            for d in b.nbr_dirs:
+                _lib.call("hx_unpack", b.field_ptr(), b.bx, b.by, b.bz, d, b.slot_ptr(p, d),
+                          c.cuda_stream)
+            mark.end("exchange", b, c)
+            ev = torch.cuda.Event()
+            ev.record(c)
+            halo_done[b.rank] = ev
+        for b in blocks:  # phase 3: interior boxes (main stream)
+            _lib.call("hx_set_device", b.device)
+            s = self.stream_of(b)
+            inner, _ = self.boxes(b)
+            rp = self._res_ptr(b, it, residual)
+            mark.begin("sweep", b, s)
+            mark.begin("interior", b, s)
+            self._box(b, inner, rp, s)
+            mark.end("interior", b, s)
+        for b in blocks:  # phase 4: wait for the halo, boundary slabs
+            _lib.call("hx_set_device", b.device)
+            s = self.stream_of(b)
+            _, shells = self.boxes(b)
+            rp = self._res_ptr(b, it, residual)
+            mark.begin("exposed", b, s)
+            if b.rank in halo_done:
+                s.wait_event(halo_done[b.rank])
+            mark.end("exposed", b, s)
+            mark.begin("shell", b, s)
+            for box in shells:
+                self._box(b, box, rp, s)
+            mark.end("shell", b, s)
+            mark.end("sweep", b, s)
+            b.cur ^= 1
         self.it += 1
 
     def run(self, iters: int, residual: bool = False) -> None:

@@ -27,11 +27,13 @@ def main():
     dims = tuple(int(x) for x in sys.argv[1:4])
     iters = int(sys.argv[4])
     out = sys.argv[5]
+    overlap = len(sys.argv) > 6 and sys.argv[6] == "1"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: r, dist=dist, timeout_s=20)
+    eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: r, dist=dist, timeout_s=20,
+                     overlap=overlap)
     eng.run(iters, residual=True)
     eng.check_errors()
     mine = (rank, eng.interior_host(rank), eng.residuals(rank))

@@ -24,13 +24,14 @@ needs2 = pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
 
 @needs2
 @pytest.mark.parametrize("pes", [2, 4, 8])
-def test_p2p_engine_across_gpus(cuda, pes):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_p2p_engine_across_gpus(cuda, pes, overlap):
     from oracle import jacobi_np
     from paper_2102_12416_b200.halo import HaloJacobi
 
     dims = (32, 32, 32)
     n = ngpu()
-    eng = HaloJacobi(dims, pes, device_of=lambda r: r % n, timeout_s=20)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: r % n, timeout_s=20, overlap=overlap)
     eng.run(20)
     eng.check_errors()
     want, _ = jacobi_np.sequential(dims, 20)
@@ -39,12 +40,14 @@ def test_p2p_engine_across_gpus(cuda, pes):
 
 
 @needs2
-def test_ipc_engine_under_torchrun(cuda, tmp_path):
+@pytest.mark.parametrize("overlap", [0, 1])
+def test_ipc_engine_under_torchrun(cuda, tmp_path, overlap):
     out = tmp_path / "verdict.json"
     n = 4 if ngpu() >= 4 else 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", "29533",
-           os.path.join(ROOT, "tests", "mp_halo_worker.py"), "48", "32", "40", "15", str(out)]
+           "--master-addr", "127.0.0.1", "--master-port", str(29533 + overlap),
+           os.path.join(ROOT, "tests", "mp_halo_worker.py"), "48", "32", "40", "15", str(out),
+           str(overlap)]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     v = json.loads(out.read_text())

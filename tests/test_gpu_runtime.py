@@ -75,10 +75,11 @@ def test_cli_csv(pkg, tmp_path):
 @pytest.mark.parametrize("pes,dims,iters", [(1, (16, 16, 16), 5), (2, (16, 16, 16), 5),
                                             (4, (16, 16, 16), 5), (8, (16, 16, 16), 5),
                                             (2, (32, 32, 32), 20), (4, (32, 32, 32), 20)])
-def test_halo_engine_matches_reference(pkg, pes, dims, iters):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_halo_engine_matches_reference(pkg, pes, dims, iters, overlap):
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi(dims, pes, device_of=lambda r: 0)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, overlap=overlap)
     eng.run(iters)
     eng.check_errors()
     key = f"{dims[0]}x{dims[1]}x{dims[2]}/{iters}/{pes}/channel-device"
@@ -87,12 +88,14 @@ def test_halo_engine_matches_reference(pkg, pes, dims, iters):
     eng.close()
 
 
-def test_halo_engine_64_cubed_8_blocks_residuals(pkg):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_halo_engine_64_cubed_8_blocks_residuals(pkg, overlap):
     """Config C1 at 8 blocks: field sha and the full residual history
-    (max over blocks) equal the reference's sequential oracle."""
+    (max over blocks) equal the reference's sequential oracle — with and
+    without the interior/boundary overlap split."""
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi((64, 64, 64), 8, device_of=lambda r: 0)
+    eng = HaloJacobi((64, 64, 64), 8, device_of=lambda r: 0, overlap=overlap)
     eng.run(100, residual=True)
     eng.check_errors()
     g = GOLD["seq_64_100"]
@@ -128,7 +131,7 @@ def test_halo_engine_b200_policy_and_odd_sizes(pkg):
     from paper_2102_12416_b200.halo import HaloJacobi
 
     dims = (24, 18, 30)
-    eng = HaloJacobi(dims, 6, device_of=lambda r: 0, policy="b200")
+    eng = HaloJacobi(dims, 6, device_of=lambda r: 0, policy="b200", overlap=True)
     eng.run(9)
     eng.check_errors()
     want, _ = jacobi_np.sequential(dims, 9)
