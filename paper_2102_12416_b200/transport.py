@@ -170,7 +170,7 @@ class Worker:
         self._fired.append((handle, comp))
 
     def _after(self, event, fn) -> None:
-        self._inflight.append(_Inflight(event, fn))
+        self._inflight.append(_Inflight(event.acquire(), fn))
 
     # ---------------------------------------------------------------- sends
 
@@ -199,8 +199,7 @@ class Worker:
         if nbytes <= self.cfg.eager_threshold:
             ready, keep = None, None
             if isinstance(source, DeviceRegion):
-                ready = torch.cuda.Event()
-                ready.record(self.space.stream_of(source.buffer.owner))
+                ready = self.space.record(source.buffer.owner)
                 direct = Frame(FRAME_EAGER, tag, nbytes, source, ready, self.id)
                 if peer._match_now(direct):
                     # the receive was already posted: one direct HBM/NVLink
@@ -211,14 +210,14 @@ class Worker:
                     self.stats["sends"] += 1
                     self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
                     return
+                ready.release()
                 source, ready, keep = self._snapshot(source)
             frame = Frame(FRAME_EAGER, tag, nbytes, source, ready, self.id, keepalive=keep)
             self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
         else:
             ready = None
             if isinstance(source, DeviceRegion):
-                ready = torch.cuda.Event()
-                ready.record(self.space.stream_of(source.buffer.owner))
+                ready = self.space.record(source.buffer.owner)
             frame = Frame(FRAME_RTS, tag, nbytes, source, ready, self.id, send_completion=completion)
             if isinstance(source, DeviceRegion) and peer._match_now(frame):
                 self.stats["tx_rts"] += 1
@@ -246,16 +245,14 @@ class Worker:
         return False
 
     def _snapshot(self, src: DeviceRegion):
-        """Stream-ordered copy of an eager device payload into a bounce buffer."""
+        """Stream-ordered copy of an eager device payload into a pooled
+        bounce buffer (returned to the pool once the receiver has read it)."""
         buf = src.buffer
-        s = self.space.stream_of(buf.owner)
-        with torch.cuda.stream(s):
-            bounce = torch.empty(max(src.size, 1), dtype=torch.uint8, device=f"cuda:{buf.gpu}")
-        _lib.call("hx_set_device", buf.gpu)
+        bounce = self.space.bounce(buf.gpu, src.size)
+        h = self.space.handle_of(buf.owner)
         if src.size:
-            _lib.call("hx_memcpy", bounce.data_ptr(), src.addr, src.size, s.cuda_stream)
-        ev = torch.cuda.Event()
-        ev.record(s)
+            _lib.call("hx_memcpy", bounce.data_ptr(), src.addr, src.size, h)
+        ev = self.space.record(buf.owner)
         return _Bounce(bounce, src.size, buf.gpu, buf.owner), ev, bounce
 
     # ------------------------------------------------------------- receives
@@ -295,8 +292,9 @@ class Worker:
         if self._inflight:
             pending = []
             for op in self._inflight:
-                if op.event.query():
+                if op.event.done():
                     op.fn()
+                    op.event.release()
                 else:
                     pending.append(op)
             self._inflight = pending
@@ -374,6 +372,7 @@ class Worker:
             if isinstance(sink, DeviceRegion):  # host -> device (pinned H2D)
                 ev = self._h2d(sink, src)
                 self._after(ev, done)
+                ev.release()
                 send_done()
             elif sink is None:
                 done(src)
@@ -391,15 +390,18 @@ class Worker:
                     and src.buffer.owner != sink.buffer.owner):
                 # direct eager send: later work on the sender's stream must
                 # not overwrite the source before the copy has read it
-                self.space.stream_of(src.buffer.owner).wait_event(ev)
+                ev.wait_on(self.space.handle_of(src.buffer.owner))
 
             def landed(keep=keep):
                 done()
                 send_done()
+                if keep is not None:
+                    self.space.return_bounce(keep)
 
             self._after(ev, landed)
             if frame.kind == FRAME_RTS:
                 sender._after(ev, lambda: None)  # sender stays non-idle until the read ends
+            ev.release()
         else:
             ev, stage = self._d2h(src, n, frame.ready)
 
@@ -411,51 +413,48 @@ class Worker:
                     sink[:n] = data
                     done()
                 send_done()
+                if keep is not None:
+                    self.space.return_bounce(keep)
 
             self._after(ev, landed_host)
+            ev.release()
 
     # ----------------------------------------------------------- GPU copies
 
     def _d2d(self, dst: DeviceRegion, src, n: int, ready):
         """Direct HBM / NVLink peer copy on the sink owner's stream."""
         owner = dst.buffer.owner
-        s = self.space.stream_of(owner)
+        h = self.space.handle_of(owner)
         if ready is not None:
-            s.wait_event(ready)
-        _lib.call("hx_set_device", dst.buffer.gpu)
-        if n:
-            _lib.call("hx_memcpy", dst.addr, src.addr, n, s.cuda_stream)
-        ev = torch.cuda.Event()
-        ev.record(s)
+            ready.wait_on(h)
+            ready.release()
+        if n:  # cudaMemcpyAsync runs on the stream's device; no set_device needed
+            _lib.call("hx_memcpy", dst.addr, src.addr, n, h)
+        ev = self.space.record(owner)
         self.stats["d2d_copies"] += 1
         self.stats["d2d_bytes"] += n
         return ev
 
     def _h2d(self, dst: DeviceRegion, data: bytes):
-        s = self.space.stream_of(dst.buffer.owner)
+        h = self.space.handle_of(dst.buffer.owner)
         stage = torch.empty(max(len(data), 1), dtype=torch.uint8, pin_memory=True)
         stage.numpy()[: len(data)] = np.frombuffer(data, dtype=np.uint8)
-        _lib.call("hx_set_device", dst.buffer.gpu)
         if data:
-            _lib.call("hx_memcpy", dst.addr, stage.data_ptr(), len(data), s.cuda_stream)
-        ev = torch.cuda.Event()
-        ev.record(s)
+            _lib.call("hx_memcpy", dst.addr, stage.data_ptr(), len(data), h)
+        ev = self.space.record(dst.buffer.owner)
         self._after(ev, lambda stage=stage: None)  # keep the staging alive until landed
         return ev
 
     def _d2h(self, src, n: int, ready):
-        gpu = src.gpu if isinstance(src, _Bounce) else src.buffer.gpu
         owner = src.owner if isinstance(src, _Bounce) else src.buffer.owner
-        s = self.space.stream_of(owner)
+        h = self.space.handle_of(owner)
         if ready is not None:
-            s.wait_event(ready)
+            ready.wait_on(h)
+            ready.release()
         stage = torch.empty(max(n, 1), dtype=torch.uint8, pin_memory=True)
-        _lib.call("hx_set_device", gpu)
         if n:
-            _lib.call("hx_memcpy", stage.data_ptr(), src.addr, n, s.cuda_stream)
-        ev = torch.cuda.Event()
-        ev.record(s)
-        return ev, stage
+            _lib.call("hx_memcpy", stage.data_ptr(), src.addr, n, h)
+        return self.space.record(owner), stage
 
     def close(self) -> None:
         pass
