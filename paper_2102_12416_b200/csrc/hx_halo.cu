@@ -189,8 +189,29 @@ __global__ void __launch_bounds__(256) copy_window_kernel(char *dst, const char 
                                                           int count) {
     const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
     const size_t nth = (size_t)gridDim.x * blockDim.x;
-    // loads bypass L1 (ld.cg): a pulled source must cross NVLink every time
-    for (int m = 0; m < count; ++m) copy_bytes(dst, src, n, tid, nth, true);
+    if ((((uintptr_t)dst | (uintptr_t)src | n) & 15) != 0) {
+        for (int m = 0; m < count; ++m) copy_bytes(dst, src, n, tid, nth, true);
+        return;
+    }
+    // The window is one flat stream of count * n/16 vectors: every thread
+    // keeps 4 independent 16-byte loads in flight whatever the message size
+    // (loads bypass L1 so a pulled source crosses NVLink every time).
+    const size_t nv = n / 16, total = nv * (size_t)count;
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    const uint4 *s = reinterpret_cast<const uint4 *>(src);
+    for (size_t base = tid; base < total; base += 4 * nth) {
+        uint4 v[4];
+        size_t at[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const size_t g = base + u * nth;
+            at[u] = g < total ? g % nv : 0;
+            if (g < total) v[u] = __ldcg(s + at[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (base + u * nth < total) d[at[u]] = v[u];
+    }
 }
 
 __device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long *p) {
