@@ -256,7 +256,9 @@ class HaloJacobi:
                   self.stream_of(b).cuda_stream)
         b.cur ^= 1
 
-    def _res_ptr(self, b: HaloBlock, it: int, residual: bool):
+    def _res_ptr(self, b: HaloBlock, it: int, residual):
+        if isinstance(residual, dict):  # explicit per-block device u64 slots
+            return residual.get(b.rank)
         if not residual:
             return None
         buf = self._res.setdefault(b.rank, [])
@@ -264,9 +266,11 @@ class HaloJacobi:
             buf.append(torch.zeros(1, dtype=torch.int64, device=f"cuda:{b.device}"))
         return buf[it].data_ptr()
 
-    def step(self, residual: bool = False, timing: dict | None = None) -> None:
+    def step(self, residual=False, timing: dict | None = None) -> None:
         """One iteration on every local block (enqueue only, no host sync).
 
+        residual: False, True (per-step device slots, see residuals()) or a
+        dict rank -> device u64 pointer accumulating max|nxt-cur|.
         timing (optional): dict of lists receiving CUDA event pairs per block
         — 'exchange' (put + wait + unpack), 'sweep' (all stencil work), and in
         overlap mode 'interior', 'exposed' (main stream stalled on the halo)
@@ -423,26 +427,22 @@ class HaloJacobi:
                 up = torch.cuda.Event()
                 up.record(cs)
                 st["uploaded"][b.rank] = up
-        for b in blocks:
-            if b.nbr_dirs:
-                _lib.call("hx_set_device", b.device)
-                self._put(b, it)
-        for b in blocks:
-            if b.nbr_dirs:
-                _lib.call("hx_set_device", b.device)
-                self._wait(b, it)
+        slots = {}
         for b in blocks:
             _lib.call("hx_set_device", b.device)
             s = self.stream_of(b)
             up = st["uploaded"].pop(b.rank, None)
             if up is not None:
-                s.wait_event(up)
+                s.wait_event(up)  # the sweep reads the uploaded ghost plane
             ring = st["ring"][b.rank]
             slot = it % ring.numel()
             if slot == 0:
                 with torch.cuda.stream(s):
                     ring.zero_()
-            self._relax(b, ring.data_ptr() + 8 * slot)
+            slots[b.rank] = ring.data_ptr() + 8 * slot
+        self.step(residual=slots)  # same (overlapped) sequence as step()
+        for b in blocks:
+            s = self.stream_of(b)
             done = torch.cuda.Event()
             done.record(s)
             st["sweep_done"][(b.rank, it)] = done
@@ -450,9 +450,8 @@ class HaloJacobi:
             if res_out is not None:
                 cs = st["copy"][b.device]
                 cs.wait_event(done)
-                _lib.call("hx_memcpy", res_out.data_ptr() + 8 * blocks.index(b),
-                          ring.data_ptr() + 8 * slot, 8, cs.cuda_stream)
-        self.it += 1
+                _lib.call("hx_memcpy", res_out.data_ptr() + 8 * blocks.index(b), slots[b.rank], 8,
+                          cs.cuda_stream)
 
     def drain_e2e(self) -> None:
         st = self._e2e_state()

@@ -106,12 +106,13 @@ def test_halo_engine_64_cubed_8_blocks_residuals(pkg, overlap):
     eng.close()
 
 
-def test_halo_engine_host_buffer_steps_match(pkg):
+@pytest.mark.parametrize("overlap", [False, True])
+def test_halo_engine_host_buffer_steps_match(pkg, overlap):
     """step_e2e (per-step pinned H2D of the hot wall, D2H of the residual)
     produces the reference's bits and residual history."""
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi((64, 64, 64), 2, device_of=lambda r: 0)
+    eng = HaloJacobi((64, 64, 64), 2, device_of=lambda r: 0, overlap=overlap)
     assert eng.grid == (1, 1, 2)
     wall = torch.ones(66 * 34, dtype=torch.float64, pin_memory=True)
     host = torch.zeros(100, 2, dtype=torch.int64, pin_memory=True)
