@@ -199,6 +199,9 @@ def main() -> int:
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--policy", choices=("b200", "reference"), default="b200",
+                    help="block decomposition: reference = cl/jacobi3d.py:62-76 exactly; b200 = "
+                         "same face area, ties broken away from splitting z (strided faces)")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: interior sweep concurrent with the halo exchange (default)")
     args = ap.parse_args()
@@ -230,7 +233,8 @@ def main() -> int:
         scaling = "weak"
         workload = f"Jacobi3D {args.block}^3 per GPU fp64 weak scaling"
     eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: local,
-                     dist=dist if world > 1 else None, overlap=bool(args.overlap))
+                     dist=dist if world > 1 else None, overlap=bool(args.overlap),
+                     policy=args.policy)
     b = eng.blocks[rank]
     s = eng.stream_of(b)
 
@@ -299,7 +303,7 @@ def main() -> int:
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
             "config": {"workload": workload,
-                       "global_dims": list(dims), "grid": list(eng.grid),
+                       "global_dims": list(dims), "grid": list(eng.grid), "policy": args.policy,
                        "block": [b.bx, b.by, b.bz], "parallelism": f"3d-blocks x{world}",
                        "l2": f"inputs > L2 (2 x {(b.bx + 2) * (b.by + 2) * (b.bz + 2) * 8 / 1e9:.1f} GB "
                              "fields per GPU vs 126 MB L2), no flush needed"},

@@ -417,7 +417,7 @@ class HaloJacobi:
                     raise ValueError(f"host_wall must hold {(b.by + 2) * (b.bz + 2)} fp64 values")
                 if not host_wall.is_pinned():
                     raise ValueError("host_wall must be pinned host memory")
-                cs = st["copy"][b.device]
+                cs = st["up"][b.device]
                 prev = st["sweep_done"].get((b.rank, it - 2))
                 if prev is not None:
                     cs.wait_event(prev)
@@ -448,14 +448,14 @@ class HaloJacobi:
             st["sweep_done"][(b.rank, it)] = done
             st["sweep_done"].pop((b.rank, it - 3), None)
             if res_out is not None:
-                cs = st["copy"][b.device]
-                cs.wait_event(done)
+                cs = st["down"][b.device]  # separate from the upload stream, which
+                cs.wait_event(done)        # must not queue behind this sweep
                 _lib.call("hx_memcpy", res_out.data_ptr() + 8 * blocks.index(b), slots[b.rank], 8,
                           cs.cuda_stream)
 
     def drain_e2e(self) -> None:
         st = self._e2e_state()
-        for cs in st["copy"].values():
+        for cs in list(st["up"].values()) + list(st["down"].values()):
             cs.synchronize()
         self.synchronize()
 
@@ -463,7 +463,8 @@ class HaloJacobi:
         st = getattr(self, "_e2e", None)
         if st is None:
             st = self._e2e = {
-                "copy": {d: torch.cuda.Stream(device=d) for d in self.streams},
+                "up": {d: torch.cuda.Stream(device=d) for d in self.streams},
+                "down": {d: torch.cuda.Stream(device=d) for d in self.streams},
                 "ring": {r: torch.zeros(4096, dtype=torch.int64, device=f"cuda:{b.device}")
                          for r, b in self.blocks.items()},
                 "sweep_done": {}, "uploaded": {},
