@@ -100,7 +100,8 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz,
                    unsigned long long *res, void *stream);
 /* Force a kernel variant (testing / profiling): 0 auto, 1 TMA pipeline,
  * 2 generic, 3 flattened slab (auto for boxes thinner than 8 rows or 16
- * columns — the overlap split's boundary shell). Returns the previous one. */
+ * columns — the overlap split's boundary shell), 4 single z column with
+ * aligned quad loads (auto for one-column boxes). Returns the previous one. */
 int hx_stencil_set_variant(int variant);
 int hx_stencil_last_variant(void);
 /* Tuning knob for the TMA pipeline: x planes per CTA work item (0 = auto). */

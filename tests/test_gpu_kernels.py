@@ -136,12 +136,38 @@ def test_box_plus_shells_equal_full_sweep(hx, variant):
     nxt0 = rng.standard_normal(cur.shape)
     n = dev(nxt0)
     for box in [inner] + slabs:
-        hx.raw("hx_stencil_set_variant")(variant if box is inner else 2)
+        hx.raw("hx_stencil_set_variant")(variant if box is inner else 0)
         hx.call("hx_stencil_box", c.data_ptr(), n.data_ptr(), bx, by, bz, *box, None, stream())
     hx.raw("hx_stencil_set_variant")(0)
     want = nxt0.copy()
     jacobi_np.stencil(cur, want)
     assert n.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("shape,kcol", [((20, 70, 66), 1), ((20, 70, 66), 66), ((9, 40, 130), 2),
+                                         ((9, 40, 130), 129), ((3, 33, 6), 6)])
+def test_z_column_kernel(hx, shape, kcol):
+    """Variant 4 (one z column, aligned quad loads + lane shuffles) over
+    every j, including warp edges and partial warps, with the residual."""
+    rng = np.random.default_rng(kcol)
+    bx, by, bz = shape
+    cur = rng.standard_normal((bx + 2, by + 2, bz + 2))
+    nxt0 = rng.standard_normal(cur.shape)
+    c, n = dev(cur), dev(nxt0)
+    r = torch.zeros(1, dtype=torch.int64, device="cuda")
+    hx.raw("hx_stencil_set_variant")(4)
+    try:
+        hx.call("hx_stencil_box", c.data_ptr(), n.data_ptr(), bx, by, bz, 1, bx + 1, 1, by + 1,
+                kcol, kcol + 1, r.data_ptr(), stream())
+    finally:
+        hx.raw("hx_stencil_set_variant")(0)
+    full = nxt0.copy()
+    jacobi_np.stencil(cur, full)
+    want = nxt0.copy()
+    want[1:-1, 1:-1, kcol] = full[1:-1, 1:-1, kcol]
+    assert n.cpu().numpy().tobytes() == want.tobytes()
+    delta = np.abs(full[1:-1, 1:-1, kcol] - cur[1:-1, 1:-1, kcol]).max()
+    assert float(r.cpu().numpy().view(np.float64)[0]) == delta
 
 
 def test_sequential_64_cubed_matches_reference_golden(hx):
