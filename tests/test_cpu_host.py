@@ -66,18 +66,26 @@ def test_decompose_neighbors_match_reference():
             assert neighbor_table(grid, r) == want
 
 
-def test_b200_policy_keeps_area_and_avoids_z():
-    from paper_2102_12416_b200.jacobi3d import decompose, decompose_b200, internal_face_area
+def test_b200_policy_minimises_weighted_face_cost():
+    from paper_2102_12416_b200.jacobi3d import (_triples, decompose, decompose_b200,
+                                                weighted_face_cost)
 
-    for dims in ((64, 64, 64), (128, 64, 64), (3072, 3072, 3072), (96, 48, 24)):
+    for dims in ((64, 64, 64), (128, 64, 64), (3072, 3072, 3072), (96, 48, 24), (3072, 1536, 1536)):
         for n in (1, 2, 4, 8, 16):
             try:
                 a, b = decompose(dims, n), decompose_b200(dims, n)
             except Exception:
                 continue
-            assert internal_face_area(dims, a) == internal_face_area(dims, b)
-    assert decompose((64, 64, 64), 2) == (1, 1, 2)       # reference: splits z
-    assert decompose_b200((64, 64, 64), 2) == (2, 1, 1)  # B200: splits x instead
+            assert weighted_face_cost(dims, b) <= weighted_face_cost(dims, a)
+            legal = [g for g in _triples(n) if all(dims[i] % g[i] == 0 for i in range(3))]
+            assert weighted_face_cost(dims, b) == min(weighted_face_cost(dims, g) for g in legal)
+    # the bench configurations
+    assert decompose_b200((3072, 1536, 1536), 2) == (2, 1, 1)
+    assert decompose_b200((3072, 3072, 1536), 4) == (2, 2, 1)
+    assert decompose_b200((3072, 3072, 3072), 4) == (2, 2, 1)   # reference: (1, 2, 2)
+    assert decompose_b200((3072, 3072, 3072), 8) == (4, 2, 1)   # reference: (2, 2, 2)
+    assert decompose((64, 64, 64), 2) == (1, 1, 2)              # reference splits z
+    assert decompose_b200((64, 64, 64), 2) == (2, 1, 1)
 
 
 def test_config_rejects_virtual_time():

@@ -127,6 +127,20 @@ def test_halo_engine_host_buffer_steps_match(pkg, overlap):
     eng.close()
 
 
+@pytest.mark.parametrize("overlap", [False, True])
+def test_halo_engine_b200_policy_8_blocks(pkg, overlap):
+    """The 8-GPU bench layout under the B200 policy ((4,2,1), no z split)
+    gives the reference's bits (decomposition invariance)."""
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi((32, 32, 32), 8, device_of=lambda r: 0, policy="b200", overlap=overlap)
+    assert eng.grid == (4, 2, 1)
+    eng.run(20)
+    eng.check_errors()
+    assert sha(eng.assemble()) == GOLD["seq_sha256"]["32x32x32/20"]
+    eng.close()
+
+
 def test_halo_engine_b200_policy_and_odd_sizes(pkg):
     from oracle import jacobi_np
     from paper_2102_12416_b200.halo import HaloJacobi
