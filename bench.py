@@ -202,6 +202,9 @@ def main() -> int:
     ap.add_argument("--policy", choices=("b200", "reference"), default="b200",
                     help="block decomposition: reference = cl/jacobi3d.py:62-76 exactly; b200 = "
                          "same face area, ties broken away from splitting z (strided faces)")
+    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
+                    help="p2p: persistent NVLink channels (the product); nccl: grouped NCCL "
+                         "send/recv comparison (implies --overlap 0)")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: interior sweep concurrent with the halo exchange (default)")
     args = ap.parse_args()
@@ -233,8 +236,9 @@ def main() -> int:
         scaling = "weak"
         workload = f"Jacobi3D {args.block}^3 per GPU fp64 weak scaling"
     eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: local,
-                     dist=dist if world > 1 else None, overlap=bool(args.overlap),
-                     policy=args.policy)
+                     dist=dist if world > 1 else None,
+                     overlap=bool(args.overlap) and args.exchange == "p2p",
+                     policy=args.policy, exchange=args.exchange if world > 1 else "p2p")
     b = eng.blocks[rank]
     s = eng.stream_of(b)
 
@@ -277,7 +281,8 @@ def main() -> int:
     else:
         sten_ms = mean_ms("sweep")
         exposed_ms = max_over_ranks(mean_ms("exchange"))
-        launches_per_step = 1 + (2 if b.nbr_dirs else 0)
+        per_face = 2 * len(b.nbr_dirs)  # nccl: pack + unpack per face (+ NCCL's own kernels)
+        launches_per_step = 1 + (per_face if eng.exchange == "nccl" else (2 if b.nbr_dirs else 0))
     xch_ms = max_over_ranks(mean_ms("exchange"))
     launches = args.steps * launches_per_step * world
     cells = b.cells
@@ -304,6 +309,7 @@ def main() -> int:
             "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
             "config": {"workload": workload,
                        "global_dims": list(dims), "grid": list(eng.grid), "policy": args.policy,
+                       "exchange": eng.exchange,
                        "block": [b.bx, b.by, b.bz], "parallelism": f"3d-blocks x{world}",
                        "l2": f"inputs > L2 (2 x {(b.bx + 2) * (b.by + 2) * (b.bz + 2) * 8 / 1e9:.1f} GB "
                              "fields per GPU vs 126 MB L2), no flush needed"},

@@ -159,9 +159,15 @@ class HaloJacobi:
     """
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
-                 policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False):
+                 policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False,
+                 exchange: str = "p2p"):
+        if exchange not in ("p2p", "nccl"):
+            raise ValueError(f"exchange must be 'p2p' or 'nccl', got {exchange!r}")
+        if exchange == "nccl" and (dist is None or overlap):
+            raise ValueError("the NCCL comparison path needs a process group and overlap=False")
         self.dims = tuple(dims)
         self.overlap = overlap
+        self.exchange = exchange
         self.pes = pes
         self.grid = (decompose if policy == "reference" else decompose_b200)(self.dims, pes)
         self.local_ranks = list(range(pes)) if local_ranks is None else list(local_ranks)
@@ -182,7 +188,10 @@ class HaloJacobi:
         self._ipc_bases = []
         self._res = {}
         self.reset()
-        self.connect()
+        if exchange == "p2p":
+            self.connect()
+        else:
+            self._nccl_buffers()
 
     # ------------------------------------------------------------ set-up --
 
@@ -275,6 +284,8 @@ class HaloJacobi:
         — 'exchange' (put + wait + unpack), 'sweep' (all stencil work), and in
         overlap mode 'interior', 'exposed' (main stream stalled on the halo)
         and 'shell'."""
+        if self.exchange == "nccl":
+            return self._step_nccl(residual, timing)
         if self.overlap:
             return self._step_overlap(residual, timing)
         it = self.it
@@ -326,6 +337,47 @@ class HaloJacobi:
         if box[0] < box[1] and box[2] < box[3] and box[4] < box[5]:
             _lib.call("hx_stencil_box", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz,
                       *box, res_ptr, stream.cuda_stream)
+
+    # ------------------------------------------- NCCL comparison exchange --
+
+    def _nccl_buffers(self) -> None:
+        self._sbuf, self._rbuf = {}, {}
+        for r, b in self.blocks.items():
+            dev = torch.device("cuda", b.device)
+            self._sbuf[r] = {d: torch.empty(b.face_elems[d], dtype=torch.float64, device=dev)
+                             for d in b.nbr_dirs}
+            self._rbuf[r] = {d: torch.empty(b.face_elems[d], dtype=torch.float64, device=dev)
+                             for d in b.nbr_dirs}
+
+    def _step_nccl(self, residual, timing) -> None:
+        """Baseline exchange (the north star's comparison point): pack into
+        local buffers, grouped NCCL send/recv (batch_isend_irecv), unpack,
+        sweep — the way a framework without persistent channels does it."""
+        it = self.it
+        mark = _Marks(timing)
+        for b in self.blocks.values():
+            s = self.stream_of(b)
+            _lib.call("hx_set_device", b.device)
+            with torch.cuda.stream(s):
+                if b.nbr_dirs:
+                    mark.begin("exchange", b, s)
+                    for d in b.nbr_dirs:
+                        _lib.call("hx_pack", b.field_ptr(), b.bx, b.by, b.bz, d,
+                                  self._sbuf[b.rank][d].data_ptr(), s.cuda_stream)
+                    ops = []
+                    for d in b.nbr_dirs:
+                        ops.append(self.dist.P2POp(self.dist.isend, self._sbuf[b.rank][d], b.neighbors[d]))
+                        ops.append(self.dist.P2POp(self.dist.irecv, self._rbuf[b.rank][d], b.neighbors[d]))
+                    for w in self.dist.batch_isend_irecv(ops):
+                        w.wait()
+                    for d in b.nbr_dirs:
+                        _lib.call("hx_unpack", b.field_ptr(), b.bx, b.by, b.bz, d,
+                                  self._rbuf[b.rank][d].data_ptr(), s.cuda_stream)
+                    mark.end("exchange", b, s)
+                mark.begin("sweep", b, s)
+                self._relax(b, self._res_ptr(b, it, residual))
+                mark.end("sweep", b, s)
+        self.it += 1
 
     def _step_overlap(self, residual: bool, timing) -> None:
         """Interior sweep concurrent with the halo exchange (paper §4.3's
