@@ -292,6 +292,19 @@ def main() -> int:
     achieved = ALG_BYTES_PER_CELL * cells / (sten_ms * 1e-3) / 1e9
     face_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs)
 
+    # ---- the exchange alone (not sharing HBM with an interior sweep): a few
+    # untimed-for-value steps with the overlap split off, for the NVLink fraction
+    iso_ms = None
+    if world > 1 and eng.exchange == "p2p":
+        saved, eng.overlap = eng.overlap, False
+        iso: dict = {}
+        for _ in range(5):
+            eng.step(timing=iso)
+        barrier()
+        eng.overlap = saved
+        pairs = iso.get("exchange", [])
+        iso_ms = max_over_ranks(statistics.median(a.elapsed_time(z) for a, z in pairs)) if pairs else None
+
     # ---- end to end through the public API with host buffers
     e2e = None
     if not args.no_e2e:
@@ -323,7 +336,11 @@ def main() -> int:
                       "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS,
                       "overlap": eng.overlap, "exposed_ms": exposed_ms,
                       "interior_ms": mean_ms("interior"), "shell_ms": mean_ms("shell"),
-                      "non_overlapped_frac": exposed_ms / (t_ms / args.steps)} if world > 1 else None),
+                      "non_overlapped_frac": exposed_ms / (t_ms / args.steps),
+                      "isolated_exchange_ms": iso_ms,
+                      "isolated_exchange_gbs": (face_bytes / (iso_ms * 1e-3) / 1e9) if iso_ms else None,
+                      "isolated_nvlink_frac": (face_bytes / (iso_ms * 1e-3) / 1e9 / NVLINK_GBS)
+                      if iso_ms else None} if world > 1 else None),
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

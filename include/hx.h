@@ -130,10 +130,10 @@ int hx_unpack(double *field, int bx, int by, int bz, int d, const double *src, v
 /* Fused multi-face pack + put + signal (Channel.send of every halo face,
  * cl/jacobi3d.py:250-253, without per-message metadata): for each d in
  * dir_mask, pack face d into dst[d] (typically the neighbour's receive slot,
- * peer-mapped) and, once every CTA of that face has stored, publish
- * *flag[d] = value with system-scope release. counters: 6 device uint32,
- * zero-initialised once; the kernel returns them to zero. flag[d] may be
- * NULL (no signal). */
+ * peer-mapped) and, once every CTA of the (persistent) grid has stored,
+ * publish every *flag[d] = value with system-scope release. counters: device
+ * uint32 scratch (6 reserved, counters[0] used), zero-initialised once; the
+ * kernel returns it to zero. flag[d] may be NULL (no signal). */
 int hx_pack_put(const double *field, int bx, int by, int bz, int dir_mask,
                 double *const dst[6], unsigned long long *const flag[6],
                 unsigned long long value, unsigned int *counters, void *stream);

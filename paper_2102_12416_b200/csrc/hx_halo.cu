@@ -63,19 +63,37 @@ __device__ __forceinline__ void copy_segment(const FaceJob &J, int row, int c0, 
     const double *cside = PACK ? J.dst + crow + c0 : J.src + crow + c0;
     if ((((uintptr_t)cside) & 15) == 0) {
         const int npair = (c1 - c0) >> 1;
-        for (int p = threadIdx.x; p < npair; p += blockDim.x) {
-            const int c = c0 + 2 * p;
-            const size_t fa = frow + (size_t)c * f.col_stride, fb = fa + f.col_stride;
-            if (PACK) {
-                double2 v;
-                v.x = LD_CG ? __ldcg(J.src + fa) : J.src[fa];
-                v.y = LD_CG ? __ldcg(J.src + fb) : J.src[fb];
-                *reinterpret_cast<double2 *>(J.dst + crow + c) = v;
-            } else {
-                const double2 *s = reinterpret_cast<const double2 *>(J.src + crow + c);
-                const double2 v = LD_CG ? __ldcg(s) : *s;
-                J.dst[fa] = v.x;
-                J.dst[fb] = v.y;
+        constexpr int U = 4;  // loads of U pairs in flight before their stores
+        for (int p0 = threadIdx.x; p0 < npair; p0 += U * blockDim.x) {
+            double2 v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int p = p0 + u * blockDim.x;
+                if (p < npair) {
+                    const int c = c0 + 2 * p;
+                    if (PACK) {
+                        const size_t fa = frow + (size_t)c * f.col_stride;
+                        v[u].x = LD_CG ? __ldcg(J.src + fa) : J.src[fa];
+                        v[u].y = LD_CG ? __ldcg(J.src + fa + f.col_stride) : J.src[fa + f.col_stride];
+                    } else {
+                        const double2 *s = reinterpret_cast<const double2 *>(J.src + crow + c);
+                        v[u] = LD_CG ? __ldcg(s) : *s;
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int p = p0 + u * blockDim.x;
+                if (p < npair) {
+                    const int c = c0 + 2 * p;
+                    if (PACK) {
+                        *reinterpret_cast<double2 *>(J.dst + crow + c) = v[u];
+                    } else {
+                        const size_t fa = frow + (size_t)c * f.col_stride;
+                        J.dst[fa] = v[u].x;
+                        J.dst[fa + f.col_stride] = v[u].y;
+                    }
+                }
             }
         }
         c0 += 2 * npair;  // odd tail (at most one element)
@@ -90,56 +108,71 @@ __device__ __forceinline__ void copy_segment(const FaceJob &J, int row, int c0, 
     }
 }
 
+// All kernels below walk the batch's work units — (face, row, column
+// segment) — with a grid-stride loop over a persistent grid of about two
+// CTAs per SM, so short face rows do not pay one CTA launch (and, for puts,
+// one system fence) each.
+__device__ __forceinline__ void unit_of(const FaceBatch &b, int unit, int &q, int &row, int &c0,
+                                        int &c1) {
+    q = find_job(b, unit);
+    const FaceJob &J = b.job[q];
+    const int local = unit - J.first_block;
+    row = local / J.col_blocks;
+    c0 = (local % J.col_blocks) * FACE_COLS_PER_BLOCK;
+    c1 = min(c0 + FACE_COLS_PER_BLOCK, J.f.cols);
+}
+
 template <bool PACK>
 __global__ void __launch_bounds__(FACE_THREADS)
 face_copy_kernel(FaceBatch b) {
-    const int q = find_job(b, blockIdx.x);
-    const FaceJob &J = b.job[q];
-    const int local = blockIdx.x - J.first_block;
-    const int row = local / J.col_blocks;
-    const int c0 = (local % J.col_blocks) * FACE_COLS_PER_BLOCK;
-    copy_segment<PACK, false>(J, row, c0, min(c0 + FACE_COLS_PER_BLOCK, J.f.cols));
+    for (int unit = blockIdx.x; unit < b.total_blocks; unit += gridDim.x) {
+        int q, row, c0, c1;
+        unit_of(b, unit, q, row, c0, c1);
+        copy_segment<PACK, false>(b.job[q], row, c0, c1);
+    }
 }
 
-// Fused pack + put + signal: the last CTA of each face publishes the flag.
+// Fused pack + put + signal. Each CTA stores its units, then (after a CTA
+// barrier) thread 0 issues one system-scope fence — cumulative over the
+// barrier, so it covers every thread's peer stores — and bumps the batch
+// counter; the last CTA fences again and release-stores every face's flag.
 __global__ void __launch_bounds__(FACE_THREADS)
 pack_put_kernel(FaceBatch b, unsigned long long value, unsigned int *counters) {
-    const int q = find_job(b, blockIdx.x);
-    const FaceJob &J = b.job[q];
-    const int local = blockIdx.x - J.first_block;
-    const int row = local / J.col_blocks;
-    const int c0 = (local % J.col_blocks) * FACE_COLS_PER_BLOCK;
-    copy_segment<true, false>(J, row, c0, min(c0 + FACE_COLS_PER_BLOCK, J.f.cols));
-    if (J.flag == nullptr) return;
-    // The CTA barrier orders every thread's peer stores before thread 0's
-    // system-scope fence (fences are cumulative), which precedes the counter
-    // atomic; the last CTA fences again and release-stores the flag.
+    for (int unit = blockIdx.x; unit < b.total_blocks; unit += gridDim.x) {
+        int q, row, c0, c1;
+        unit_of(b, unit, q, row, c0, c1);
+        copy_segment<true, false>(b.job[q], row, c0, c1);
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();
-        const unsigned nblk = (unsigned)(J.f.rows * J.col_blocks);
-        const unsigned done = atomicAdd(&counters[q], 1u) + 1u;
-        if (done == nblk) {
-            counters[q] = 0u;  // re-arm for the next launch (stream ordered)
+        const unsigned done = atomicAdd(&counters[0], 1u) + 1u;
+        if (done == gridDim.x) {
+            counters[0] = 0u;  // re-arm for the next launch (stream ordered)
             __threadfence_system();
-            hx::st_release_sys(J.flag, value);
+            for (int q = 0; q < b.njobs; ++q)
+                if (b.job[q].flag) hx::st_release_sys(b.job[q].flag, value);
         }
     }
 }
 
-// Fused wait + unpack: every CTA acquires its face's flag before reading.
+// Fused wait + unpack: each CTA's thread 0 acquires every face flag once,
+// then the CTA copies its units (slot reads bypass L1).
 __global__ void __launch_bounds__(FACE_THREADS)
 wait_unpack_kernel(FaceBatch b, unsigned long long value, unsigned long long timeout_ns, int *err) {
     __shared__ int ok;
-    const int q = find_job(b, blockIdx.x);
-    const FaceJob &J = b.job[q];
-    if (threadIdx.x == 0) ok = J.flag ? hx::spin_until(J.flag, value, timeout_ns, err) : 1;
+    if (threadIdx.x == 0) {
+        ok = 1;
+        for (int q = 0; q < b.njobs && ok; ++q)
+            if (b.job[q].flag) ok = hx::spin_until(b.job[q].flag, value, timeout_ns, err);
+    }
     __syncthreads();
     if (!ok) return;
-    const int local = blockIdx.x - J.first_block;
-    const int row = local / J.col_blocks;
-    const int c0 = (local % J.col_blocks) * FACE_COLS_PER_BLOCK;
-    copy_segment<false, true>(J, row, c0, min(c0 + FACE_COLS_PER_BLOCK, J.f.cols));
+    for (int unit = blockIdx.x; unit < b.total_blocks; unit += gridDim.x) {
+        int q, row, c0, c1;
+        unit_of(b, unit, q, row, c0, c1);
+        copy_segment<false, true>(b.job[q], row, c0, c1);
+    }
 }
 
 __global__ void signal_kernel(unsigned long long *flag, unsigned long long value) {
@@ -311,6 +344,24 @@ __global__ void pingpong_kernel(int role, const char *src, char *peer_dst, size_
     if (role == 0 && lead && elapsed) *elapsed = hx::globaltimer() - t0;
 }
 
+unsigned face_grid(const FaceBatch &b) {
+    static int sms = 0;
+    if (!sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (sms <= 0) sms = 148;
+    }
+    static int mult = 0;
+    if (!mult) {
+        const char *e = getenv("HX_FACE_GRID_MULT");
+        mult = e ? atoi(e) : 4;
+        if (mult <= 0) mult = 4;
+    }
+    const int cap = mult * sms;
+    return (unsigned)(b.total_blocks < cap ? (b.total_blocks > 0 ? b.total_blocks : 1) : cap);
+}
+
 int build_batch(FaceBatch &b, int bx, int by, int bz, int dir_mask, bool pack,
                 const double *field_src, double *field_dst, const double *const *src,
                 double *const *dst, unsigned long long *const *flag) {
@@ -349,7 +400,7 @@ int hx_pack(const double *field, int bx, int by, int bz, int d, double *dst, voi
     dsts[d] = dst;
     int rc = build_batch(b, bx, by, bz, 1 << d, true, field, nullptr, nullptr, dsts, nullptr);
     if (rc) return rc;
-    face_copy_kernel<true><<<b.total_blocks, FACE_THREADS, 0, (cudaStream_t)stream>>>(b);
+    face_copy_kernel<true><<<face_grid(b), FACE_THREADS, 0, (cudaStream_t)stream>>>(b);
     HX_LAUNCH_CHECK();
     return 0;
 }
@@ -361,7 +412,7 @@ int hx_unpack(double *field, int bx, int by, int bz, int d, const double *src, v
     srcs[d] = src;
     int rc = build_batch(b, bx, by, bz, 1 << d, false, nullptr, field, srcs, nullptr, nullptr);
     if (rc) return rc;
-    face_copy_kernel<false><<<b.total_blocks, FACE_THREADS, 0, (cudaStream_t)stream>>>(b);
+    face_copy_kernel<false><<<face_grid(b), FACE_THREADS, 0, (cudaStream_t)stream>>>(b);
     HX_LAUNCH_CHECK();
     return 0;
 }
@@ -377,7 +428,7 @@ int hx_pack_put(const double *field, int bx, int by, int bz, int dir_mask, doubl
     bool any_flag = false;
     for (int q = 0; q < b.njobs; ++q) any_flag |= b.job[q].flag != nullptr;
     if (any_flag && !counters) return HX_E_INVALID;
-    pack_put_kernel<<<b.total_blocks, FACE_THREADS, 0, (cudaStream_t)stream>>>(b, value, counters);
+    pack_put_kernel<<<face_grid(b), FACE_THREADS, 0, (cudaStream_t)stream>>>(b, value, counters);
     HX_LAUNCH_CHECK();
     return 0;
 }
@@ -390,7 +441,7 @@ int hx_wait_unpack(double *field, int bx, int by, int bz, int dir_mask, const do
     FaceBatch b;
     int rc = build_batch(b, bx, by, bz, dir_mask, false, nullptr, field, src, nullptr, flag);
     if (rc) return rc;
-    wait_unpack_kernel<<<b.total_blocks, FACE_THREADS, 0, (cudaStream_t)stream>>>(b, value,
+    wait_unpack_kernel<<<face_grid(b), FACE_THREADS, 0, (cudaStream_t)stream>>>(b, value,
                                                                                  timeout_ns, err);
     HX_LAUNCH_CHECK();
     return 0;
