@@ -51,6 +51,18 @@ def test_run_jacobi_all_modes_bitwise_32(pkg, pes):
         assert sha(r["field"]) == want, mode
 
 
+@pytest.mark.parametrize("pes", [1, 2, 4, 8])
+def test_run_jacobi_persistent_mode(pkg, pes):
+    """The B200 extension mode (persistent NVLink channels + overlap) through
+    the reference's own entry point gives the reference's bits."""
+    from paper_2102_12416_b200.jacobi3d import run_jacobi
+
+    r = run_jacobi(dims=(16, 16, 16), iters=5, mode="channel-persistent", pes=pes, verify=True)
+    assert sha(r["field"]) == GOLD["run_jacobi_sha256"][f"16x16x16/5/{pes}/channel-device"]
+    assert r["max_err"] == 0.0 and r["total_ns"] > 0
+    assert (r["comm_ns"] == 0.0) == (pes == 1)
+
+
 def test_single_block_verify_and_no_comm(pkg):
     from paper_2102_12416_b200.jacobi3d import run_jacobi
 
