@@ -169,6 +169,7 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
 
     double xm[PTS], x0[PTS];
     double worst = 0.0;
+    int nan_seen = 0;
     {
         const double *s0 = reinterpret_cast<const double *>(smem);
         const double *s1 = reinterpret_cast<const double *>(smem + STAGE_STRIDE);
@@ -179,9 +180,17 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
             const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
             xm[p] = s0[o];
             x0[p] = s1[o];
+            nan_seen |= (xm[p] != xm[p]) | (x0[p] != x0[p]);
         }
     }
-    __syncthreads();  // plane 0 lives in registers now: recycle its stage
+    // Plane 0 must be in registers before its stage is recycled. A plain
+    // bar.sync does not wait for this warp's outstanding shared loads (it
+    // blocks lazily), and the refill below is an async-proxy write: under SM
+    // contention the TMA can land before a queued LDS is served. The
+    // barrier's predicate consumes every loaded value, so each warp's loads
+    // have completed when it arrives. (Inside the loop the loaded values feed
+    // the stores that precede the barrier, which orders them the same way.)
+    (void)__syncthreads_or(nan_seen);
     if (threadIdx.x == 0 && NSTAGE < nplanes) {
         hx::mbar_expect_tx(&bar[0], STAGE_BYTES);
         hx::tma_load_3d(smem, &map, kload, jb - 1, ib - 1 + NSTAGE, &bar[0]);

@@ -271,3 +271,36 @@ def test_medium_block_vs_threaded_c_oracle(hx):
         jacobi_c.stencil(h_cur, h_nxt)
         h_cur, h_nxt = h_nxt, h_cur
     assert c.cpu().numpy().tobytes() == h_cur.tobytes()
+
+
+@pytest.mark.parametrize("k0", [1, 2])
+def test_tma_stencil_under_concurrent_face_traffic(hx, k0):
+    """Regression: face kernels on a second (high-priority) stream while the
+    TMA stencil sweeps must not perturb its output. Before the prologue
+    barrier consumed its shared loads, SM contention let the stage-0 refill
+    overwrite plane 0 under a still-queued LDS (wrong first plane of a
+    chunk, thousands of cells per 20 sweeps at this size)."""
+    n = 512
+    g = torch.Generator(device="cuda").manual_seed(3)
+    cur = torch.randn((n + 2,) * 3, dtype=torch.float64, device="cuda", generator=g)
+    other = torch.randn_like(cur)
+    slot = torch.zeros(n * n * 6, dtype=torch.float64, device="cuda")
+    box = (1, n + 1, 1, n + 1, k0, n + 1)
+    hx.raw("hx_stencil_set_variant")(1)
+    ref = torch.zeros_like(cur)
+    hx.call("hx_stencil_box", cur.data_ptr(), ref.data_ptr(), n, n, n, *box, None, stream())
+    torch.cuda.synchronize()
+    S, C = torch.cuda.Stream(), torch.cuda.Stream(priority=-1)
+    bad = 0
+    for _ in range(12):
+        out = torch.zeros_like(cur)
+        torch.cuda.synchronize()
+        for _ in range(8):
+            for d in range(6):
+                hx.call("hx_pack", other.data_ptr(), n, n, n, d, slot.data_ptr(), C.cuda_stream)
+                hx.call("hx_unpack", other.data_ptr(), n, n, n, d, slot.data_ptr(), C.cuda_stream)
+        hx.call("hx_stencil_box", cur.data_ptr(), out.data_ptr(), n, n, n, *box, None, S.cuda_stream)
+        torch.cuda.synchronize()
+        bad += int((out != ref).sum().item())
+    hx.raw("hx_stencil_set_variant")(0)
+    assert bad == 0

@@ -153,6 +153,25 @@ def test_halo_engine_b200_policy_8_blocks(pkg, overlap):
     eng.close()
 
 
+@pytest.mark.parametrize("pes,policy", [(2, "reference"), (2, "b200"), (4, "reference")])
+def test_halo_engine_overlap_at_scale(pkg, pes, policy):
+    """Bench-sized blocks (512^3 split 2 or 4 ways), overlap on: the comm
+    stream's face kernels share SMs with the TMA interior sweep for 30
+    iterations, and the field must still equal the single-block sweep bit
+    for bit (the small-size tests finish before kernels ever co-reside)."""
+    from paper_2102_12416_b200.halo import HaloJacobi
+    from paper_2102_12416_b200.jacobi3d import sequential_oracle
+
+    dims = (512, 512, 512)
+    want, _ = sequential_oracle(dims, 30)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, policy=policy, overlap=True)
+    eng.run(30)
+    eng.check_errors()
+    got = eng.assemble()
+    eng.close()
+    assert np.array_equal(got, want), int((got != want).sum())
+
+
 def test_halo_engine_b200_policy_and_odd_sizes(pkg):
     from oracle import jacobi_np
     from paper_2102_12416_b200.halo import HaloJacobi
