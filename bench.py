@@ -202,9 +202,11 @@ def main() -> int:
     ap.add_argument("--policy", choices=("b200", "reference"), default="b200",
                     help="block decomposition: reference = cl/jacobi3d.py:62-76 exactly; b200 = "
                          "same face area, ties broken away from splitting z (strided faces)")
-    ap.add_argument("--exchange", choices=("p2p", "nccl"), default="p2p",
-                    help="p2p: persistent NVLink channels (the product); nccl: grouped NCCL "
-                         "send/recv comparison (implies --overlap 0)")
+    ap.add_argument("--exchange", choices=("p2p", "fused", "nccl"), default="fused",
+                    help="p2p: persistent NVLink channels (pack+put / wait+unpack kernels); "
+                         "fused: the boundary sweep stores into the neighbours' ghost planes "
+                         "itself (hx_shell_put); nccl: grouped NCCL send/recv comparison "
+                         "(implies --overlap 0)")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: interior sweep concurrent with the halo exchange (default)")
     args = ap.parse_args()
@@ -274,10 +276,16 @@ def main() -> int:
         return statistics.mean(a.elapsed_time(z) for a, z in pairs) if pairs else 0.0
 
     t_ms = max_over_ranks(start.elapsed_time(stop))
-    if eng.overlap and b.nbr_dirs:
-        sten_ms = mean_ms("interior") + mean_ms("shell")  # the sweep kernels, not the wait
+    sweep_cells = b.cells  # cells the timed TMA launch relaxes
+    if (eng.overlap or eng.exchange == "fused") and b.nbr_dirs:
+        inner = eng.boxes(b)[0]
+        sweep_cells = (inner[1] - inner[0]) * (inner[3] - inner[2]) * (inner[5] - inner[4])
+        sten_ms = mean_ms("interior")  # the TMA interior launch alone
         exposed_ms = max_over_ranks(mean_ms("exposed"))
-        launches_per_step = 1 + len(eng.boxes(b)[1]) + 1 + 2 * len(b.nbr_dirs)
+        if eng.exchange == "fused":
+            launches_per_step = 2  # interior + hx_shell_put
+        else:
+            launches_per_step = 1 + len(eng.boxes(b)[1]) + 1 + 2 * len(b.nbr_dirs)
     else:
         sten_ms = mean_ms("sweep")
         exposed_ms = max_over_ranks(mean_ms("exchange"))
@@ -289,7 +297,7 @@ def main() -> int:
     total_cells = cells * world
     value = total_cells * args.steps / (t_ms * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
-    achieved = ALG_BYTES_PER_CELL * cells / (sten_ms * 1e-3) / 1e9
+    achieved = ALG_BYTES_PER_CELL * sweep_cells / (sten_ms * 1e-3) / 1e9
     face_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs)
 
     # ---- the exchange alone (not sharing HBM with an interior sweep): a few
@@ -330,7 +338,7 @@ def main() -> int:
                          "frac": achieved / peak, "traffic": ncu_traffic(),
                          "kernel": "stencil_tma_kernel", "peak_kind": peak_kind,
                          "kernel_ms": sten_ms,
-                         "alg_bytes_per_launch": ALG_BYTES_PER_CELL * cells},
+                         "alg_bytes_per_launch": ALG_BYTES_PER_CELL * sweep_cells},
             "halo": ({"bytes_out_per_rank": face_bytes, "exchange_ms": xch_ms,
                       "exchange_gbs": face_bytes / (xch_ms * 1e-3) / 1e9,
                       "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS,

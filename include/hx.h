@@ -146,6 +146,28 @@ int hx_wait_unpack(double *field, int bx, int by, int bz, int dir_mask,
                    unsigned long long value, unsigned long long timeout_ns, int *err,
                    void *stream);
 
+/* Fused boundary sweep + halo put (HaloJacobi exchange="fused"; replaces
+ * the pack -> Channel.send -> recv -> unpack_all chain of Block.run,
+ * cl/jacobi3d.py:246-257, and the boundary part of _BlockCore.update,
+ * cl/jacobi3d.py:165-173). Each CTA first waits until every non-NULL
+ * wait_flag[d] >= wait_value (the neighbours' boundary of the previous
+ * iteration is in cur's ghost planes and they are done reading ours; bounded
+ * by timeout_ns, then *err = HX_E_TIMEOUT). It then relaxes the nbox
+ * (<= 6) boxes `boxes[6*q .. 6*q+5]` = i0,i1,j0,j1,k0,k1 of cur into nxt
+ * and stores every cell lying on the plane facing d (i == 1 for d = 0,
+ * i == bx for d = 1, ... k == bz for d = 5) also into remote[d], the
+ * neighbour's nxt array of the same padded shape, at its ghost cell. After
+ * the last CTA's stores are visible system-wide it release-stores
+ * signal_value into every non-NULL signal_flag[d] (skipped if *err != 0).
+ * counter: one zero-initialised uint32 that the kernel returns to zero.
+ * res: optional max|nxt-cur| accumulator, as for hx_stencil. */
+int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbox,
+                 const int *boxes, double *const remote[6],
+                 unsigned long long *const wait_flag[6], unsigned long long wait_value,
+                 unsigned long long *const signal_flag[6], unsigned long long signal_value,
+                 unsigned int *counter, unsigned long long timeout_ns, int *err,
+                 unsigned long long *res, void *stream);
+
 /* ---------------------------------------------------------------- flags --
  * Persistent-channel completion words (the Channel API's per-direction
  * counter, cl/channels.py:75-99, carried as a 64-bit flag value). */

@@ -31,7 +31,8 @@ EXPORTS = (
     "hx_enable_peer", "hx_ipc_get", "hx_ipc_open", "hx_ipc_close", "hx_memcpy",
     "hx_memcpy_peer", "hx_copy_sm", "hx_copy_sm_window", "hx_fill_f64", "hx_stencil", "hx_stencil_box",
     "hx_stencil_set_variant", "hx_stencil_last_variant", "hx_stencil_set_chunk", "hx_div6_check",
-    "hx_init_block", "hx_pack", "hx_unpack", "hx_pack_put", "hx_wait_unpack", "hx_signal",
+    "hx_init_block", "hx_pack", "hx_unpack", "hx_pack_put", "hx_wait_unpack", "hx_shell_put",
+    "hx_signal",
     "hx_wait_flag", "hx_read_u64", "hx_pingpong", "hx_pingpong_ll",
 )
 
@@ -102,6 +103,8 @@ _SIGS = {
     "hx_pack_put": ([_V, _I, _I, _I, _I, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64, _V, _V], _I),
     "hx_wait_unpack": ([_V, _I, _I, _I, _I, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64, _U64,
                         _V, _V], _I),
+    "hx_shell_put": ([_V, _V, _I, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64,
+                      ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V], _I),
     "hx_signal": ([_V, _U64, _V], _I),
     "hx_wait_flag": ([_V, _U64, _U64, _V, _V], _I),
     "hx_read_u64": ([_V, ctypes.POINTER(_U64)], _I),

@@ -294,6 +294,89 @@ __global__ void init_block_kernel(double *f, int bx, int by, int bz, int hot_wal
     }
 }
 
+// ------------------------------------------- fused boundary sweep + put ---
+// The halo exchange folded into the stencil that produces it (exchange
+// "fused"): the boundary boxes of a block are relaxed here, and every cell
+// that lies on a neighbour-facing plane is stored twice — into our nxt and,
+// over NVLink, straight into the neighbour's nxt ghost plane, where its
+// next sweep reads it. No pack, no staging slot, no unpack: the face bytes
+// leave the SM once. One flag per direction orders everything: the
+// neighbour's release of flag = it+1 (after its boundary sweep of it-1)
+// says both "your ghost plane holds my boundary of it-1" and "I have
+// finished reading the ghost plane you are about to overwrite".
+struct ShellJob {
+    int nbox;
+    int box[6][6];          // i0,i1,j0,j1,k0,k1 (1-based, half-open)
+    long long start[7];     // prefix cell counts
+    double *remote[6];      // neighbour's nxt base (same padded shape), or null
+    long long shift[6];     // our padded offset + shift[d] = its ghost cell
+    int face[6];            // coordinate of our plane facing d (i/j/k by d/2)
+    unsigned long long *wait[6];
+    unsigned long long *signal[6];
+};
+
+__global__ void __launch_bounds__(256)
+shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
+                 ShellJob J, unsigned long long wait_value, unsigned long long signal_value,
+                 unsigned *counter, unsigned long long timeout_ns, int *err,
+                 unsigned long long *res) {
+    __shared__ int ok;
+    if (threadIdx.x == 0) {
+        ok = 1;
+        for (int d = 0; d < 6 && ok; ++d)
+            if (J.wait[d]) ok = hx::spin_until(J.wait[d], wait_value, timeout_ns, err);
+    }
+    __syncthreads();
+    const hx::Geom g(by, bz);
+    const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
+    double worst = 0.0;
+    const long long n = J.start[J.nbox];
+    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; ok && q < n;
+         q += (long long)gridDim.x * blockDim.x) {
+        int b = 0;
+        while (q >= J.start[b + 1]) ++b;
+        const int *x = J.box[b];
+        const long long r = q - J.start[b];
+        const int nj = x[3] - x[2], nk = x[5] - x[4];
+        int i, j, k;
+        if (nk > 1) {  // rows along k: coalesced
+            k = x[4] + (int)(r % nk);
+            const long long t = r / nk;
+            j = x[2] + (int)(t % nj);
+            i = x[0] + (int)(t / nj);
+        } else {       // a z column: run along j
+            k = x[4];
+            j = x[2] + (int)(r % nj);
+            i = x[0] + (int)(r / nj);
+        }
+        const size_t c = g.at(i, j, k);
+        // Coherent (not .nc) loads: ghost cells were stored by a peer GPU
+        // while this kernel may already have been running; the flag acquire
+        // above (observed through the barrier) orders these loads after them.
+        const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy], cur[c - 1],
+                                   cur[c + 1]));
+        nxt[c] = v;
+        if (res) worst = fmax(worst, fabs(__dsub_rn(v, cur[c])));
+        const int coord[3] = {i, j, k};
+#pragma unroll
+        for (int d = 0; d < 6; ++d)
+            if (J.remote[d] && coord[d >> 1] == J.face[d]) J.remote[d][(long long)c + J.shift[d]] = v;
+    }
+    if (res) cta_max_to_global(worst, res);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // this CTA's local + remote stores, system-wide
+        const unsigned done = atomicAdd(counter, 1u) + 1u;
+        if (done == gridDim.x) {
+            *counter = 0u;  // re-arm (launches on one stream are ordered)
+            __threadfence_system();
+            const bool healthy = !err || *(volatile int *)err == 0;
+            for (int d = 0; d < 6 && healthy; ++d)
+                if (J.signal[d]) hx::st_release_sys(J.signal[d], signal_value);
+        }
+    }
+}
+
 __global__ void fill_kernel(double *p, size_t n, double v) {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
          q += (size_t)gridDim.x * blockDim.x)
@@ -572,6 +655,54 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
     }
     g_last_variant = 2;
     return launch_generic(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);
+}
+
+int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbox,
+                 const int *boxes, double *const remote[6], unsigned long long *const wait_flag[6],
+                 unsigned long long wait_value, unsigned long long *const signal_flag[6],
+                 unsigned long long signal_value, unsigned int *counter,
+                 unsigned long long timeout_ns, int *err, unsigned long long *res, void *stream) {
+    if (!cur || !nxt || !counter || bx < 1 || by < 1 || bz < 1 || nbox < 0 || nbox > 6)
+        return HX_E_INVALID;
+    if (nbox > 0 && !boxes) return HX_E_INVALID;
+    ShellJob J;
+    memset(&J, 0, sizeof(J));
+    const long long sx = (long long)(by + 2) * (bz + 2), sy = bz + 2;
+    const long long step[3] = {sx * bx, sy * by, (long long)bz};
+    const int ext[3] = {bx, by, bz};
+    for (int d = 0; d < 6; ++d) {
+        J.remote[d] = remote ? remote[d] : nullptr;
+        J.wait[d] = wait_flag ? wait_flag[d] : nullptr;
+        J.signal[d] = signal_flag ? signal_flag[d] : nullptr;
+        // our plane 1 (d even) is the neighbour's ghost plane ext+1, our
+        // plane ext (d odd) its ghost plane 0
+        J.face[d] = (d & 1) ? ext[d >> 1] : 1;
+        J.shift[d] = (d & 1) ? -step[d >> 1] : step[d >> 1];
+    }
+    J.start[0] = 0;
+    for (int q = 0; q < nbox; ++q) {
+        const int *x = boxes + 6 * q;
+        if (x[0] < 1 || x[2] < 1 || x[4] < 1 || x[1] > bx + 1 || x[3] > by + 1 || x[5] > bz + 1)
+            return HX_E_INVALID;
+        const long long cells = (long long)std::max(0, x[1] - x[0]) * std::max(0, x[3] - x[2]) *
+                                std::max(0, x[5] - x[4]);
+        for (int e = 0; e < 6; ++e) J.box[J.nbox][e] = x[e];
+        if (cells == 0) continue;
+        J.start[J.nbox + 1] = J.start[J.nbox] + cells;
+        ++J.nbox;
+    }
+    const long long n = J.start[J.nbox];
+    static int mult = 0;
+    if (!mult) {
+        const char *e = getenv("HX_SHELL_GRID_MULT");  // CTAs per SM (tuning)
+        mult = e && atoi(e) > 0 ? atoi(e) : 2;
+    }
+    const unsigned grid = (unsigned)std::max<long long>(
+        1, std::min<long long>((n + 255) / 256, (long long)mult * num_sms()));
+    shell_put_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        cur, nxt, by, bz, J, wait_value, signal_value, counter, timeout_ns, err, res);
+    HX_LAUNCH_CHECK();
+    return 0;
 }
 
 int hx_stencil(const double *cur, double *nxt, int bx, int by, int bz, unsigned long long *res,

@@ -80,6 +80,8 @@ class HaloBlock:
         # filled by HaloJacobi.connect(): (neighbour arena base, its side)
         self.put_dst = [None] * NDIRS
         self.put_flag = [None] * NDIRS
+        # exchange="fused": the neighbour's two field bases per direction
+        self.peer_fields = [None] * NDIRS
 
     @property
     def base(self) -> int:
@@ -142,10 +144,10 @@ def exchange_table(dist, mine):
     records — the one-time persistent-channel set-up. Without a process
     group every block is local and the table is just ``mine``."""
     if dist is None:
-        return {r: (h, o, dv) for (r, h, o, dv) in mine}
+        return {rec[0]: tuple(rec[1:]) for rec in mine}
     gathered = [None] * dist.get_world_size()
     dist.all_gather_object(gathered, mine)
-    return {r: (h, o, dv) for part in gathered for (r, h, o, dv) in part}
+    return {rec[0]: tuple(rec[1:]) for part in gathered for rec in part}
 
 
 class HaloJacobi:
@@ -161,8 +163,8 @@ class HaloJacobi:
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
                  policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False,
                  exchange: str = "p2p"):
-        if exchange not in ("p2p", "nccl"):
-            raise ValueError(f"exchange must be 'p2p' or 'nccl', got {exchange!r}")
+        if exchange not in ("p2p", "fused", "nccl"):
+            raise ValueError(f"exchange must be 'p2p', 'fused' or 'nccl', got {exchange!r}")
         if exchange == "nccl" and (dist is None or overlap):
             raise ValueError("the NCCL comparison path needs a process group and overlap=False")
         self.dims = tuple(dims)
@@ -188,7 +190,7 @@ class HaloJacobi:
         self._ipc_bases = []
         self._res = {}
         self.reset()
-        if exchange == "p2p":
+        if exchange in ("p2p", "fused"):
             self.connect()
         else:
             self._nccl_buffers()
@@ -214,31 +216,45 @@ class HaloJacobi:
 
     def connect(self) -> None:
         """Exchange receive-arena addresses once (the persistent channel set-up)."""
+        fused = self.exchange == "fused"
         mine = []
         for r, b in self.blocks.items():
-            handle = (ctypes.c_char * 64)()
-            off = ctypes.c_size_t(0)
-            if self.dist is not None:
-                _lib.call("hx_set_device", b.device)
-                _lib.call("hx_ipc_get", b.base, handle, ctypes.byref(off))
-            mine.append((r, bytes(handle), off.value, b.device))
+            rec = [r]
+            for ptr in [b.base] + ([f.data_ptr() for f in b.fields] if fused else []):
+                handle = (ctypes.c_char * 64)()
+                off = ctypes.c_size_t(0)
+                if self.dist is not None:
+                    _lib.call("hx_set_device", b.device)
+                    _lib.call("hx_ipc_get", ptr, handle, ctypes.byref(off))
+                rec += [bytes(handle), off.value]
+                if len(rec) == 3:
+                    rec.append(b.device)
+            mine.append(tuple(rec))
         table = exchange_table(self.dist, mine)
-        bases = {}
+        bases, fields = {}, {}
         for r, b in self.blocks.items():
             for d in b.nbr_dirs:
                 n = b.neighbors[d]
                 if n in self.blocks:
                     bases[n] = self.blocks[n].base
+                    fields[n] = [f.data_ptr() for f in self.blocks[n].fields]
                     if self.blocks[n].device != b.device:
                         _lib.call("hx_enable_peer", b.device, self.blocks[n].device)
                 elif n not in bases:
-                    h, o, _ = table[n]
-                    base = ctypes.c_void_p()
+                    rec = table[n]
                     _lib.call("hx_set_device", b.device)
-                    _lib.call("hx_ipc_open", h, ctypes.byref(base))
-                    self._ipc_bases.append(base.value)
-                    bases[n] = base.value + o
+                    bases[n] = self._open(rec[0], rec[1])
+                    if fused:
+                        fields[n] = [self._open(rec[3], rec[4]), self._open(rec[5], rec[6])]
                 b.link(d, bases[n])
+                if fused:
+                    b.peer_fields[d] = fields[n]
+
+    def _open(self, handle: bytes, offset: int) -> int:
+        base = ctypes.c_void_p()
+        _lib.call("hx_ipc_open", handle, ctypes.byref(base))
+        self._ipc_bases.append(base.value)
+        return base.value + offset
 
     # ------------------------------------------------------------- steps --
 
@@ -286,6 +302,8 @@ class HaloJacobi:
         and 'shell'."""
         if self.exchange == "nccl":
             return self._step_nccl(residual, timing)
+        if self.exchange == "fused":
+            return self._step_fused(residual, timing)
         if self.overlap:
             return self._step_overlap(residual, timing)
         it = self.it
@@ -438,6 +456,80 @@ class HaloJacobi:
             for box in shells:
                 self._box(b, box, rp, s)
             mark.end("shell", b, s)
+            mark.end("sweep", b, s)
+            b.cur ^= 1
+        self.it += 1
+
+    # ------------------------------------------------------- fused mode --
+
+    def _prime(self) -> None:
+        """Before the first fused step: one channel exchange (pack_put +
+        wait_unpack, flags -> 1) so cur's ghost planes hold the neighbours'
+        initial boundary — afterwards every boundary value travels inside
+        hx_shell_put."""
+        for b in self.blocks.values():
+            if b.nbr_dirs:
+                _lib.call("hx_set_device", b.device)
+                self._put(b, 0)
+        for b in self.blocks.values():
+            if b.nbr_dirs:
+                _lib.call("hx_set_device", b.device)
+                self._wait(b, 0)
+
+    def _step_fused(self, residual, timing) -> None:
+        """exchange="fused": per block, the comm stream runs ONE kernel that
+        waits for the neighbours' previous boundary, relaxes the boundary
+        shell and stores the neighbour-facing planes straight into the
+        neighbours' nxt ghost planes over NVLink, then releases their flags
+        (hx_shell_put); the main stream sweeps the interior concurrently.
+        The step's work is complete on the main stream (it waits for the
+        shell), so the next interior sees this step's boundary."""
+        it = self.it
+        if it == 0:
+            self._prime()
+        blocks = list(self.blocks.values())
+        mark = _Marks(timing)
+        shell_done = {}
+        for b in blocks:
+            if not b.nbr_dirs:
+                continue
+            _lib.call("hx_set_device", b.device)
+            s, c = self.stream_of(b), self.comm[b.device]
+            ready = torch.cuda.Event()
+            ready.record(s)  # the previous interior (and shell) finished
+            c.wait_event(ready)
+            _, shells = self.boxes(b)
+            flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
+            nxt = b.cur ^ 1  # every block flips in lock step: the peer's nxt too
+            remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
+            wait = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
+            signal = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+            mark.begin("exchange", b, c)
+            _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
+                      len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array(wait), it + 1,
+                      _lib.ptr_array(signal), it + 2, b.counters_ptr + 4, self.timeout_ns,
+                      b.err_ptr, self._res_ptr(b, it, residual), c.cuda_stream)
+            mark.end("exchange", b, c)
+            ev = torch.cuda.Event()
+            ev.record(c)
+            shell_done[b.rank] = ev
+        for b in blocks:
+            _lib.call("hx_set_device", b.device)
+            s = self.stream_of(b)
+            rp = self._res_ptr(b, it, residual)
+            mark.begin("sweep", b, s)
+            mark.begin("interior", b, s)
+            if b.nbr_dirs:
+                inner, _ = self.boxes(b)
+                self._box(b, inner, rp, s)
+            else:
+                _lib.call("hx_stencil", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz,
+                          rp, s.cuda_stream)
+            mark.end("interior", b, s)
+            mark.begin("exposed", b, s)
+            if b.rank in shell_done:
+                s.wait_event(shell_done[b.rank])
+            mark.end("exposed", b, s)
             mark.end("sweep", b, s)
             b.cur ^= 1
         self.it += 1

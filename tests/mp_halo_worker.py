@@ -1,6 +1,9 @@
 """torchrun worker for the multi-process (CUDA IPC) halo path.
 
-    torchrun --nproc-per-node N tests/mp_halo_worker.py DX DY DZ ITERS OUT.json
+    torchrun --nproc-per-node N tests/mp_halo_worker.py DX DY DZ ITERS OUT.json [MODE]
+
+MODE: 0 = channel exchange, 1 = channel exchange + interior overlap,
+fused = boundary sweep stores straight into the neighbours' ghost planes.
 
 One rank per GPU: HaloJacobi with local_ranks=[rank] opens its neighbours'
 receive arenas through CUDA IPC handles exchanged once over gloo, runs
@@ -27,13 +30,13 @@ def main():
     dims = tuple(int(x) for x in sys.argv[1:4])
     iters = int(sys.argv[4])
     out = sys.argv[5]
-    overlap = len(sys.argv) > 6 and sys.argv[6] == "1"
+    mode = sys.argv[6] if len(sys.argv) > 6 else "0"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: r, dist=dist, timeout_s=20,
-                     overlap=overlap)
+                     overlap=mode == "1", exchange="fused" if mode == "fused" else "p2p")
     eng.run(iters, residual=True)
     eng.check_errors()
     mine = (rank, eng.interior_host(rank), eng.residuals(rank))

@@ -24,14 +24,15 @@ needs2 = pytest.mark.skipif(ngpu() < 2, reason="needs >= 2 GPUs")
 
 @needs2
 @pytest.mark.parametrize("pes", [2, 4, 8])
-@pytest.mark.parametrize("overlap", [False, True])
-def test_p2p_engine_across_gpus(cuda, pes, overlap):
+@pytest.mark.parametrize("exchange,overlap", [("p2p", False), ("p2p", True), ("fused", False)])
+def test_p2p_engine_across_gpus(cuda, pes, exchange, overlap):
     from oracle import jacobi_np
     from paper_2102_12416_b200.halo import HaloJacobi
 
     dims = (32, 32, 32)
     n = ngpu()
-    eng = HaloJacobi(dims, pes, device_of=lambda r: r % n, timeout_s=20, overlap=overlap)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: r % n, timeout_s=20, overlap=overlap,
+                     exchange=exchange)
     eng.run(20)
     eng.check_errors()
     want, _ = jacobi_np.sequential(dims, 20)
@@ -40,14 +41,14 @@ def test_p2p_engine_across_gpus(cuda, pes, overlap):
 
 
 @needs2
-@pytest.mark.parametrize("overlap", [0, 1])
-def test_ipc_engine_under_torchrun(cuda, tmp_path, overlap):
+@pytest.mark.parametrize("mode", ["0", "1", "fused"])
+def test_ipc_engine_under_torchrun(cuda, tmp_path, mode):
     out = tmp_path / "verdict.json"
     n = 4 if ngpu() >= 4 else 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29533 + overlap),
+           "--master-addr", "127.0.0.1", "--master-port", str(29533 + ["0", "1", "fused"].index(mode)),
            os.path.join(ROOT, "tests", "mp_halo_worker.py"), "48", "32", "40", "15", str(out),
-           str(overlap)]
+           mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     v = json.loads(out.read_text())

@@ -87,11 +87,11 @@ def test_cli_csv(pkg, tmp_path):
 @pytest.mark.parametrize("pes,dims,iters", [(1, (16, 16, 16), 5), (2, (16, 16, 16), 5),
                                             (4, (16, 16, 16), 5), (8, (16, 16, 16), 5),
                                             (2, (32, 32, 32), 20), (4, (32, 32, 32), 20)])
-@pytest.mark.parametrize("overlap", [False, True])
-def test_halo_engine_matches_reference(pkg, pes, dims, iters, overlap):
+@pytest.mark.parametrize("exchange,overlap", [("p2p", False), ("p2p", True), ("fused", False)])
+def test_halo_engine_matches_reference(pkg, pes, dims, iters, exchange, overlap):
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, overlap=overlap)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, overlap=overlap, exchange=exchange)
     eng.run(iters)
     eng.check_errors()
     key = f"{dims[0]}x{dims[1]}x{dims[2]}/{iters}/{pes}/channel-device"
@@ -100,14 +100,14 @@ def test_halo_engine_matches_reference(pkg, pes, dims, iters, overlap):
     eng.close()
 
 
-@pytest.mark.parametrize("overlap", [False, True])
-def test_halo_engine_64_cubed_8_blocks_residuals(pkg, overlap):
+@pytest.mark.parametrize("exchange,overlap", [("p2p", False), ("p2p", True), ("fused", False)])
+def test_halo_engine_64_cubed_8_blocks_residuals(pkg, exchange, overlap):
     """Config C1 at 8 blocks: field sha and the full residual history
     (max over blocks) equal the reference's sequential oracle — with and
     without the interior/boundary overlap split."""
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi((64, 64, 64), 8, device_of=lambda r: 0, overlap=overlap)
+    eng = HaloJacobi((64, 64, 64), 8, device_of=lambda r: 0, overlap=overlap, exchange=exchange)
     eng.run(100, residual=True)
     eng.check_errors()
     g = GOLD["seq_64_100"]
@@ -118,13 +118,13 @@ def test_halo_engine_64_cubed_8_blocks_residuals(pkg, overlap):
     eng.close()
 
 
-@pytest.mark.parametrize("overlap", [False, True])
-def test_halo_engine_host_buffer_steps_match(pkg, overlap):
+@pytest.mark.parametrize("exchange,overlap", [("p2p", False), ("p2p", True), ("fused", False)])
+def test_halo_engine_host_buffer_steps_match(pkg, exchange, overlap):
     """step_e2e (per-step pinned H2D of the hot wall, D2H of the residual)
     produces the reference's bits and residual history."""
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi((64, 64, 64), 2, device_of=lambda r: 0, overlap=overlap)
+    eng = HaloJacobi((64, 64, 64), 2, device_of=lambda r: 0, overlap=overlap, exchange=exchange)
     assert eng.grid == (1, 1, 2)
     wall = torch.ones(66 * 34, dtype=torch.float64, pin_memory=True)
     host = torch.zeros(100, 2, dtype=torch.int64, pin_memory=True)
@@ -139,13 +139,14 @@ def test_halo_engine_host_buffer_steps_match(pkg, overlap):
     eng.close()
 
 
-@pytest.mark.parametrize("overlap", [False, True])
-def test_halo_engine_b200_policy_8_blocks(pkg, overlap):
+@pytest.mark.parametrize("exchange,overlap", [("p2p", False), ("p2p", True), ("fused", False)])
+def test_halo_engine_b200_policy_8_blocks(pkg, exchange, overlap):
     """The 8-GPU bench layout under the B200 policy ((4,2,1), no z split)
     gives the reference's bits (decomposition invariance)."""
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi((32, 32, 32), 8, device_of=lambda r: 0, policy="b200", overlap=overlap)
+    eng = HaloJacobi((32, 32, 32), 8, device_of=lambda r: 0, policy="b200", overlap=overlap,
+                     exchange=exchange)
     assert eng.grid == (4, 2, 1)
     eng.run(20)
     eng.check_errors()
@@ -154,7 +155,8 @@ def test_halo_engine_b200_policy_8_blocks(pkg, overlap):
 
 
 @pytest.mark.parametrize("pes,policy", [(2, "reference"), (2, "b200"), (4, "reference")])
-def test_halo_engine_overlap_at_scale(pkg, pes, policy):
+@pytest.mark.parametrize("exchange", ["p2p", "fused"])
+def test_halo_engine_overlap_at_scale(pkg, pes, policy, exchange):
     """Bench-sized blocks (512^3 split 2 or 4 ways), overlap on: the comm
     stream's face kernels share SMs with the TMA interior sweep for 30
     iterations, and the field must still equal the single-block sweep bit
@@ -164,7 +166,8 @@ def test_halo_engine_overlap_at_scale(pkg, pes, policy):
 
     dims = (512, 512, 512)
     want, _ = sequential_oracle(dims, 30)
-    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, policy=policy, overlap=True)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, policy=policy, overlap=exchange == "p2p",
+                     exchange=exchange)
     eng.run(30)
     eng.check_errors()
     got = eng.assemble()
@@ -172,12 +175,14 @@ def test_halo_engine_overlap_at_scale(pkg, pes, policy):
     assert np.array_equal(got, want), int((got != want).sum())
 
 
-def test_halo_engine_b200_policy_and_odd_sizes(pkg):
+@pytest.mark.parametrize("exchange", ["p2p", "fused"])
+def test_halo_engine_b200_policy_and_odd_sizes(pkg, exchange):
     from oracle import jacobi_np
     from paper_2102_12416_b200.halo import HaloJacobi
 
     dims = (24, 18, 30)
-    eng = HaloJacobi(dims, 6, device_of=lambda r: 0, policy="b200", overlap=True)
+    eng = HaloJacobi(dims, 6, device_of=lambda r: 0, policy="b200", overlap=exchange == "p2p",
+                     exchange=exchange)
     eng.run(9)
     eng.check_errors()
     want, _ = jacobi_np.sequential(dims, 9)
