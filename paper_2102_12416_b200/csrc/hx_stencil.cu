@@ -444,11 +444,20 @@ template <bool RES, int BOX_Z>
 int launch_tma_t(const CUtensorMap &map, double *nxt, int by, int bz, int i0, int i1, int j0,
                  int j1, int k0, int k1, int ntj, int ntk, int chunk, int nchunks, int grows, long items,
                  unsigned long long *res, cudaStream_t st) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    // Function attributes live in each device's context: set them once per
+    // device (a process driving several GPUs launches this on each), and ask
+    // for the full shared-memory carveout so 3 CTAs (3 x 74 KB) fit per SM.
+    static unsigned long long attr_set = 0;  // bit per device ordinal
+    int dev = 0;
+    HX_TRY(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set & bit)) {
         HX_TRY(cudaFuncSetAttribute(stencil_tma_kernel<RES, BOX_Z>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-        attr_set = true;
+        HX_TRY(cudaFuncSetAttribute(stencil_tma_kernel<RES, BOX_Z>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared));
+        attr_set |= bit;
     }
     stencil_tma_kernel<RES, BOX_Z><<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
         map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk, chunk, nchunks, grows, res);

@@ -25,7 +25,10 @@ def main():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--residual", action="store_true")
     ap.add_argument("--shape", default=None, help="bx,by,bz (default n,n,n)")
+    ap.add_argument("--device", type=int, default=0)
     args = ap.parse_args()
+    torch.cuda.set_device(args.device)
+    _lib.call("hx_set_device", args.device)
     n = args.n
     bx, by, bz = (int(x) for x in args.shape.split(",")) if args.shape else (n, n, n)
     shape = (bx + 2, by + 2, bz + 2)
