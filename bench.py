@@ -330,7 +330,7 @@ def main() -> int:
             "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
             "config": {"workload": workload,
                        "global_dims": list(dims), "grid": list(eng.grid), "policy": args.policy,
-                       "exchange": eng.exchange,
+                       "exchange": eng.exchange if world > 1 else "none (single block)",
                        "block": [b.bx, b.by, b.bz], "parallelism": f"3d-blocks x{world}",
                        "l2": f"inputs > L2 (2 x {(b.bx + 2) * (b.by + 2) * (b.bz + 2) * 8 / 1e9:.1f} GB "
                              "fields per GPU vs 126 MB L2), no flush needed"},
