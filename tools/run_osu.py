@@ -47,7 +47,7 @@ def main():
         r = measure_latency("charm-channel", "host", size, iters=lat_iters // 2, warmup=3)
         emit({**r, "level": "api", "gpus": min(ngpu, 2)})
         for api in ("charm-channel", "charm-messaging"):
-            r = measure_bandwidth(api, "device", size, window=64, iters=5, warmup=1)
+            r = measure_bandwidth(api, "device", size, window=64, iters=5, warmup=2)
             emit({**r, "level": "api", "gpus": min(ngpu, 2)})
         if ngpu >= 2:
             emit({**device_latency(size, iters=2000 if size <= 65536 else 200, warmup=50),
