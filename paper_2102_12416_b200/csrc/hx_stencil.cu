@@ -26,8 +26,8 @@
 // x+1 centre and the four y/z neighbours from shared memory. Outputs are
 // stored from registers with coalesced stores through pointers advanced
 // one plane per step. The residual max|nxt-cur| uses the register-resident
-// centre and is reduced warp -> CTA -> one atomicMax on the uint64 bit
-// pattern (valid for non-negative doubles).
+// centre and is reduced per warp into one atomicMax on the uint64 bit
+// pattern (valid for non-negative doubles), skipped when already covered.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -97,18 +97,19 @@ __device__ __forceinline__ double sum6(double xm, double xp, double ym, double y
     return __dadd_rn(t, zp);
 }
 
-__device__ __forceinline__ void cta_max_to_global(double worst, unsigned long long *res) {
-    __shared__ double red[32];
+// Residual max|nxt - cur| into one uint64 word (for non-negative doubles the
+// bit-pattern order is the value order). Warp shuffle reduction, then lane 0
+// of each warp updates the word: no CTA barrier, so the warps of a short TMA
+// work item retire independently. Every warp of a sweep targets the same
+// word, and an unconditional atomic would serialise at its L2 slice; the max
+// only grows, so lane 0 skips the atomic when the (possibly stale, hence
+// lower) current value already covers its w.
+__device__ __forceinline__ void warp_max_to_global(double worst, unsigned long long *res) {
     for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-    const int nwarps = (int)(blockDim.x * blockDim.y * blockDim.z) >> 5;
-    const int lane = tid & 31, warp = tid >> 5;
-    if (lane == 0) red[warp] = worst;
-    __syncthreads();
-    if (tid == 0) {
-        double w = red[0];
-        for (int q = 1; q < nwarps; ++q) w = fmax(w, red[q]);
-        if (w > 0.0) atomicMax(res, (unsigned long long)__double_as_longlong(w));
+    if ((tid & 31) == 0 && worst > 0.0) {
+        const unsigned long long wb = (unsigned long long)__double_as_longlong(worst);
+        if (wb > *(volatile unsigned long long *)res) atomicMax(res, wb);
     }
 }
 
@@ -238,7 +239,7 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
         }
         s_c = s_n;
     }
-    if (RES) cta_max_to_global(worst, res);
+    if (RES) warp_max_to_global(worst, res);
 }
 
 // ----------------------------------------------------------- generic ----
@@ -260,7 +261,7 @@ stencil_generic_kernel(const double *__restrict__ cur, double *__restrict__ nxt,
         nxt[c] = v;
         if (res) worst = fabs(__dsub_rn(v, __ldg(cur + c)));
     }
-    if (res) cta_max_to_global(worst, res);
+    if (res) warp_max_to_global(worst, res);
 }
 
 // Device self-check of div6 against the library division.
@@ -362,7 +363,7 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
         for (int d = 0; d < 6; ++d)
             if (J.remote[d] && coord[d >> 1] == J.face[d]) J.remote[d][(long long)c + J.shift[d]] = v;
     }
-    if (res) cta_max_to_global(worst, res);
+    if (res) warp_max_to_global(worst, res);
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence_system();  // this CTA's local + remote stores, system-wide
@@ -537,7 +538,7 @@ stencil_slab_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
         nxt[c] = v;
         if (res) worst = fmax(worst, fabs(__dsub_rn(v, __ldg(cur + c))));
     }
-    if (res) cta_max_to_global(worst, res);
+    if (res) warp_max_to_global(worst, res);
 }
 
 // One z column (k = kcol) over an (i, j) box: the z-face boundary shell of
@@ -573,7 +574,7 @@ stencil_zcol_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
         nxt[at] = v;
         if (res) worst = fabs(__dsub_rn(v, ctr));
     }
-    if (res) cta_max_to_global(worst, res);
+    if (res) warp_max_to_global(worst, res);
 }
 
 int launch_zcol(const double *cur, double *nxt, int by, int bz, int i0, int i1, int j0, int j1,
