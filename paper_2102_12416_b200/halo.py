@@ -158,11 +158,17 @@ class HaloJacobi:
     process group (None when every block is local). policy "reference"
     uses cl/jacobi3d.py's decompose (bit-for-bit the reference's block
     layout); "b200" prefers not to split z on ties.
+
+    exchange: "fused" (default) — the boundary sweep stores straight into
+    the neighbours' ghost planes (hx_shell_put) while the interior sweeps;
+    "p2p" — persistent-channel pack+put / wait+unpack kernels, with the
+    interior/boundary split when overlap=True; "nccl" — the comparison
+    path (pack, NCCL send/recv, unpack). overlap applies to "p2p" only.
     """
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
                  policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False,
-                 exchange: str = "p2p"):
+                 exchange: str = "fused"):
         if exchange not in ("p2p", "fused", "nccl"):
             raise ValueError(f"exchange must be 'p2p', 'fused' or 'nccl', got {exchange!r}")
         if exchange == "nccl" and (dist is None or overlap):

@@ -19,10 +19,10 @@ def main():
     ref, _ = sequential_oracle(dims, iters)
     ngpu = torch.cuda.device_count()
     for gpus in ([0], list(range(min(2, ngpu)))):
-        for overlap in (False, True):
+        for exchange, overlap in (("p2p", False), ("p2p", True), ("fused", False)):
             for policy in ("reference", "b200"):
                 eng = HaloJacobi(dims, 2, device_of=lambda r: gpus[r % len(gpus)], overlap=overlap,
-                                 policy=policy)
+                                 policy=policy, exchange=exchange)
                 timing = {}
                 for _ in range(iters):
                     eng.step(timing=timing if os.environ.get("TIMING") else None)
@@ -30,7 +30,7 @@ def main():
                 f = eng.assemble()
                 d = np.abs(f - ref)
                 bad = np.argwhere(d != 0)
-                print(f"gpus={gpus} overlap={overlap} policy={policy} grid={eng.grid} "
+                print(f"gpus={gpus} exchange={exchange} overlap={overlap} policy={policy} grid={eng.grid} "
                       f"max|d|={d.max():.3e} nbad={len(bad)} first={bad[:3].tolist()}", flush=True)
                 eng.close()
                 del eng

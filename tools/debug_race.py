@@ -17,9 +17,11 @@ def main():
     which = sys.argv[3] if len(sys.argv) > 3 else "both"
     engines = {}
     if which in ("both", "overlap"):
-        engines["overlap"] = HaloJacobi((n, n, n), 2, device_of=lambda r: 0, overlap=True)
+        engines["overlap"] = HaloJacobi((n, n, n), 2, device_of=lambda r: 0, overlap=True,
+                                       exchange="p2p")
     if which in ("both", "plain"):
-        engines["plain"] = HaloJacobi((n, n, n), 2, device_of=lambda r: 0, overlap=False)
+        engines["plain"] = HaloJacobi((n, n, n), 2, device_of=lambda r: 0, overlap=False,
+                                     exchange="p2p")
     grid = next(iter(engines.values())).grid
     print("grid", grid, flush=True)
     seq = [torch.empty((n + 2,) * 3, dtype=torch.float64, device="cuda") for _ in range(2)]

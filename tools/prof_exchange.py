@@ -24,7 +24,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     args = ap.parse_args()
     n = args.n
-    eng = HaloJacobi((2 * n, n, n), 2, device_of=lambda r: r, timeout_s=20)
+    eng = HaloJacobi((2 * n, n, n), 2, device_of=lambda r: r, timeout_s=20, exchange="p2p")
     put_ms, wait_ms, both_ms = [], [], []
     for rep in range(args.reps + 2):
         ev = {}
