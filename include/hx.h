@@ -78,6 +78,15 @@ int hx_ipc_close(void *base);
 int hx_memcpy(void *dst, const void *src, size_t bytes, void *stream);          /* cudaMemcpyDefault */
 int hx_memcpy_peer(void *dst, int dst_dev, const void *src, int src_dev, size_t bytes, void *stream);
 int hx_copy_sm(void *dst, const void *src, size_t bytes, void *stream);         /* SM-issued (peer ok) */
+/* The transport's per-message device move in one call (Worker._d2d, the
+ * B200 replacement of the PULL/PAYLOAD byte moves at cl/transport.py:284-289,
+ * 430-432, 449-465): stream waits for ready_event (if given), copies bytes
+ * (<= HX_MOVE_SM_MAX as an SM kernel on `device`, the stream's GPU; larger
+ * on the copy engines), records done_event, and makes order_stream (if
+ * given) wait for it. The current device is left unchanged. */
+#define HX_MOVE_SM_MAX (64u << 10)
+int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream,
+            void *ready_event, void *done_event, void *order_stream);
 /* count back-to-back copies src -> dst in one launch (OSU window). */
 int hx_copy_sm_window(void *dst, const void *src, size_t bytes, int count, void *stream);
 int hx_fill_f64(double *dst, size_t n, double value, void *stream);

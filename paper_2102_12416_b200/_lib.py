@@ -29,7 +29,7 @@ EXPORTS = (
     "hx_event_query", "hx_event_synchronize", "hx_event_elapsed_ms", "hx_stream_wait_event",
     "hx_malloc", "hx_free", "hx_malloc_host", "hx_free_host", "hx_can_access_peer",
     "hx_enable_peer", "hx_ipc_get", "hx_ipc_open", "hx_ipc_close", "hx_memcpy",
-    "hx_memcpy_peer", "hx_copy_sm", "hx_copy_sm_window", "hx_fill_f64", "hx_stencil", "hx_stencil_box",
+    "hx_memcpy_peer", "hx_copy_sm", "hx_move", "hx_copy_sm_window", "hx_fill_f64", "hx_stencil", "hx_stencil_box",
     "hx_stencil_set_variant", "hx_stencil_last_variant", "hx_stencil_set_chunk", "hx_div6_check",
     "hx_init_block", "hx_pack", "hx_unpack", "hx_pack_put", "hx_wait_unpack", "hx_shell_put",
     "hx_signal",
@@ -89,6 +89,7 @@ _SIGS = {
     "hx_memcpy": ([_V, _V, _SZ, _V], _I),
     "hx_memcpy_peer": ([_V, _I, _V, _I, _SZ, _V], _I),
     "hx_copy_sm": ([_V, _V, _SZ, _V], _I),
+    "hx_move": ([_V, _V, _SZ, _I, _V, _V, _V, _V], _I),
     "hx_copy_sm_window": ([_V, _V, _SZ, _I, _V], _I),
     "hx_fill_f64": ([_V, _SZ, _D, _V], _I),
     "hx_stencil": ([_V, _V, _I, _I, _I, _V, _V], _I),

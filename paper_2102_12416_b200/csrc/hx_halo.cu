@@ -491,6 +491,31 @@ int hx_copy_sm(void *dst, const void *src, size_t bytes, void *stream) {
     return 0;
 }
 
+int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream, void *ready_event,
+            void *done_event, void *order_stream) {
+    if (bytes && (!dst || !src)) return HX_E_INVALID;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (ready_event) HX_TRY(cudaStreamWaitEvent(st, (cudaEvent_t)ready_event, 0));
+    if (bytes > HX_MOVE_SM_MAX) {
+        HX_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, st));
+    } else if (bytes) {
+        // a launch costs the host less than a peer cudaMemcpyAsync; kernels
+        // launch on the current device, so switch to the stream's and back
+        int prev = 0;
+        HX_TRY(cudaGetDevice(&prev));
+        if (prev != device) HX_TRY(cudaSetDevice(device));
+        const unsigned grid = (unsigned)std::max<size_t>(1, std::min<size_t>((bytes / 16 + 255) / 256, 64));
+        copy_kernel<<<grid, 256, 0, st>>>((char *)dst, (const char *)src, bytes);
+        const cudaError_t e = cudaGetLastError();
+        if (prev != device) cudaSetDevice(prev);
+        if (e != cudaSuccess) return (int)e;
+    }
+    if (done_event) HX_TRY(cudaEventRecord((cudaEvent_t)done_event, st));
+    if (order_stream && done_event)
+        HX_TRY(cudaStreamWaitEvent((cudaStream_t)order_stream, (cudaEvent_t)done_event, 0));
+    return 0;
+}
+
 int hx_copy_sm_window(void *dst, const void *src, size_t bytes, int count, void *stream) {
     if (!bytes || count <= 0) return 0;
     if (!dst || !src) return HX_E_INVALID;

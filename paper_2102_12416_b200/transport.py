@@ -52,6 +52,8 @@ class StartupError(TransportError):
 FRAME_EAGER = 0
 FRAME_RTS = 1
 _NAMES = {FRAME_EAGER: "eager", FRAME_RTS: "rts"}
+_TX_KEY = {k: f"tx_{v}" for k, v in _NAMES.items()}
+_RX_KEY = {k: f"rx_{v}" for k, v in _NAMES.items()}
 
 
 class Frame:
@@ -224,7 +226,7 @@ class Worker:
                 self.stats["tx_direct"] += 1
                 self.stats["sends"] += 1
                 return
-        self.stats[f"tx_{_NAMES[frame.kind]}"] += 1
+        self.stats[_TX_KEY[frame.kind]] += 1
         self.stats["sends"] += 1
         peer.inbound.append(frame)
 
@@ -232,14 +234,14 @@ class Worker:
         """Receiver side of a direct send: if a posted receive matches and no
         earlier frame from the same sender is still queued (FIFO per pair) or
         parked by a hold predicate, absorb the frame immediately."""
-        if self.hold is not None or any(f.src == frame.src for f in self.inbound):
+        if self.hold is not None or (self.inbound and any(f.src == frame.src for f in self.inbound)):
             return False
         for i, req in enumerate(self.posted):
             if req.matches(frame.tag):
                 del self.posted[i]
                 frame.seq = self._arrival_seq
                 self._arrival_seq += 1
-                self.stats[f"rx_{_NAMES[frame.kind]}"] += 1
+                self.stats[_RX_KEY[frame.kind]] += 1
                 self._absorb(req, frame)
                 return True
         return False
@@ -249,10 +251,9 @@ class Worker:
         bounce buffer (returned to the pool once the receiver has read it)."""
         buf = src.buffer
         bounce = self.space.bounce(buf.gpu, src.size)
-        h = self.space.handle_of(buf.owner)
-        if src.size:
-            _lib.call("hx_memcpy", bounce.data_ptr(), src.addr, src.size, h)
-        ev = self.space.record(buf.owner)
+        ev = self.space.event(buf.gpu)
+        _lib.call("hx_move", bounce.data_ptr(), src.addr, src.size, buf.gpu,
+                  self.space.handle_of(buf.owner), None, ev.ptr, None)
         return _Bounce(bounce, src.size, buf.gpu, buf.owner), ev, bounce
 
     # ------------------------------------------------------------- receives
@@ -321,7 +322,7 @@ class Worker:
     def _arrived(self, frame: Frame) -> None:
         frame.seq = self._arrival_seq
         self._arrival_seq += 1
-        self.stats[f"rx_{_NAMES[frame.kind]}"] += 1
+        self.stats[_RX_KEY[frame.kind]] += 1
         for i, req in enumerate(self.posted):
             if req.matches(frame.tag):
                 del self.posted[i]
@@ -384,13 +385,14 @@ class Worker:
             return
         # device source: the sender's region (rdv) or a bounce snapshot (eager)
         if isinstance(sink, DeviceRegion):
-            ev = self._d2d(sink, src, n, frame.ready)
-            keep = frame.keepalive
+            order = None
             if (frame.kind == FRAME_EAGER and isinstance(src, DeviceRegion)
                     and src.buffer.owner != sink.buffer.owner):
                 # direct eager send: later work on the sender's stream must
                 # not overwrite the source before the copy has read it
-                ev.wait_on(self.space.handle_of(src.buffer.owner))
+                order = self.space.handle_of(src.buffer.owner)
+            ev = self._d2d(sink, src, n, frame.ready, order)
+            keep = frame.keepalive
 
             def landed(keep=keep):
                 done()
@@ -421,16 +423,16 @@ class Worker:
 
     # ----------------------------------------------------------- GPU copies
 
-    def _d2d(self, dst: DeviceRegion, src, n: int, ready):
-        """Direct HBM / NVLink peer copy on the sink owner's stream."""
-        owner = dst.buffer.owner
-        h = self.space.handle_of(owner)
+    def _d2d(self, dst: DeviceRegion, src, n: int, ready, order=None):
+        """Direct HBM / NVLink peer copy on the sink owner's stream: wait for
+        the source, copy, record completion (and, if ``order`` is a stream,
+        order it behind the copy) in one libhx call (hx_move)."""
+        buf = dst.buffer
+        ev = self.space.event(buf.gpu)
+        _lib.call("hx_move", dst.addr, src.addr, n, buf.gpu, self.space.handle_of(buf.owner),
+                  ready.ptr if ready is not None else None, ev.ptr, order)
         if ready is not None:
-            ready.wait_on(h)
             ready.release()
-        if n:  # cudaMemcpyAsync runs on the stream's device; no set_device needed
-            _lib.call("hx_memcpy", dst.addr, src.addr, n, h)
-        ev = self.space.record(owner)
         self.stats["d2d_copies"] += 1
         self.stats["d2d_bytes"] += n
         return ev
