@@ -107,10 +107,14 @@ int hx_stencil(const double *cur, double *nxt, int bx, int by, int bz,
 int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz,
                    int i0, int i1, int j0, int j1, int k0, int k1,
                    unsigned long long *res, void *stream);
-/* Force a kernel variant (testing / profiling): 0 auto, 1 TMA pipeline,
+/* Force a kernel variant (testing / profiling): 0 auto, 1 TMA pipeline
+ * (auto when the padded row pitch is a multiple of 16 bytes, i.e. even bz),
  * 2 generic, 3 flattened slab (auto for boxes thinner than 8 rows or 16
  * columns — the overlap split's boundary shell), 4 single z column with
- * aligned quad loads (auto for one-column boxes). Returns the previous one. */
+ * aligned quad loads (auto for one-column boxes), 5 row-bulk-copy pipeline
+ * (the TMA kernel's schedule, rows staged by non-tensor bulk copies; auto
+ * for odd bz, whose row pitch a tensor map cannot describe).
+ * Returns the previous one. */
 int hx_stencil_set_variant(int variant);
 int hx_stencil_last_variant(void);
 /* Tuning knob for the TMA pipeline: x planes per CTA work item (0 = auto). */

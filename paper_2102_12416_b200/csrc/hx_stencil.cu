@@ -113,6 +113,67 @@ __device__ __forceinline__ void warp_max_to_global(double worst, unsigned long l
     }
 }
 
+// One x plane of a tile from two staged planes: P0 holds plane q (y/z
+// neighbours), PP plane q+1; xm/x0 carry planes q-1 and q in registers and
+// are advanced. Stores the live cells of plane q and folds their residual.
+// ylo / yhi: distance from a cell to its y-1 / y+1 neighbour in P0 (the row
+// pitch, or pitch -+ 1 when rows are staged with alternating alignment).
+template <bool RES, int BOX_Z>
+__device__ __forceinline__ void relax_plane(const double *P0, const double *PP, int soff, int ylo,
+                                            int yhi, double (&xm)[PTS], double (&x0)[PTS],
+                                            double *out, int bz, unsigned live, double &worst) {
+    double v[PTS];
+    bool fast = true;
+#pragma unroll
+    for (int p = 0; p < PTS; ++p) {
+        const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
+        const double xp = PP[o];
+        v[p] = sum6(xm[p], xp, P0[o - ylo], P0[o + yhi], P0[o - 1], P0[o + 1]);
+        xm[p] = x0[p];
+        x0[p] = xp;
+        fast &= div6_fast_ok(v[p]);
+    }
+    if (fast) {
+#pragma unroll
+        for (int p = 0; p < PTS; ++p) v[p] = div6_fast(v[p]);
+    } else {
+#pragma unroll
+        for (int p = 0; p < PTS; ++p) v[p] = div6(v[p]);
+    }
+#pragma unroll
+    for (int p = 0; p < PTS; ++p) {
+        if (live & (1u << p)) {
+            out[(size_t)((p >> 1) * NWARP) * (bz + 2) + 32 * (p & 1)] = v[p];
+            if (RES) worst = fmax(worst, fabs(__dsub_rn(v[p], xm[p])));
+        }
+    }
+}
+
+// Work item = (tile j, tile k, x chunk) in grouped order: groups of `grows`
+// tile rows; inside a group all tiles of chunk c, then chunk c+1, ...
+// Concurrent CTAs therefore cover adjacent tiles of the same few planes
+// (tile halos hit L2) and chunk c+1 of a tile starts while chunk c's last
+// planes are still in L2.
+struct Item {
+    int jb, kb, ib, nplanes;
+};
+
+__device__ __forceinline__ Item work_item(int j0, int k0, int i0, int i1, int ntj, int ntk,
+                                          int chunk, int nchunks, int grows) {
+    const int items_g = grows * ntk * nchunks;
+    const int g = blockIdx.x / items_g;
+    const int rem = blockIdx.x - g * items_g;
+    const int tiles_g = min(grows, ntj - g * grows) * ntk;
+    const int c = rem / tiles_g;
+    const int t = rem - c * tiles_g;
+    Item it;
+    it.jb = j0 + (g * grows + t / ntk) * TY;
+    it.kb = k0 + (t % ntk) * TZ;
+    it.ib = i0 + c * chunk;
+    it.nplanes = min(it.ib + chunk, i1) - it.ib + 2;  // padded planes ib-1 .. ie
+    return it;
+}
+
 // ------------------------------------------------------- TMA pipeline ----
 // Work item = (tile j, tile k, x chunk). Box in interior coordinates:
 // [i0,i1) x [j0,j1) x [k0,k1).
@@ -125,22 +186,8 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
 
-    // Work order: groups of `grows` tile rows; inside a group all tiles of
-    // chunk c, then chunk c+1, ... Concurrent CTAs therefore cover adjacent
-    // tiles of the same few planes (tile halos hit L2) and chunk c+1 of a
-    // tile starts while chunk c's last planes are still in L2.
-    const int items_g = grows * ntk * nchunks;
-    const int g = blockIdx.x / items_g;
-    const int rem = blockIdx.x - g * items_g;
-    const int tiles_g = min(grows, ntj - g * grows) * ntk;
-    const int c = rem / tiles_g;
-    const int t = rem - c * tiles_g;
-    const int tj = g * grows + t / ntk;
-    const int tk = t % ntk;
-    const int jb = j0 + tj * TY, kb = k0 + tk * TZ;
-    const int ib = i0 + c * chunk;
-    const int ie = min(ib + chunk, i1);
-    const int nplanes = ie - ib + 2;  // padded planes ib-1 .. ie
+    const Item it = work_item(j0, k0, i0, i1, ntj, ntk, chunk, nchunks, grows);
+    const int jb = it.jb, kb = it.kb, ib = it.ib, nplanes = it.nplanes;
     const int kshift = BOX_Z == TZ + 2 ? 0 : (kb - 1) & 1;  // 16-byte aligned TMA rows
     const int kload = kb - 1 - kshift;
 
@@ -200,33 +247,9 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     for (int q = 1; q <= nplanes - 2; ++q) {
         const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;  // stage holding plane q+1
         hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
-        const double *P0 = reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE);
-        const double *PP = reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE);
-        double v[PTS];
-        bool fast = true;
-#pragma unroll
-        for (int p = 0; p < PTS; ++p) {
-            const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
-            const double xp = PP[o];
-            v[p] = sum6(xm[p], xp, P0[o - BOX_Z], P0[o + BOX_Z], P0[o - 1], P0[o + 1]);
-            xm[p] = x0[p];
-            x0[p] = xp;
-            fast &= div6_fast_ok(v[p]);
-        }
-        if (fast) {
-#pragma unroll
-            for (int p = 0; p < PTS; ++p) v[p] = div6_fast(v[p]);
-        } else {
-#pragma unroll
-            for (int p = 0; p < PTS; ++p) v[p] = div6(v[p]);
-        }
-#pragma unroll
-        for (int p = 0; p < PTS; ++p) {
-            if (live & (1u << p)) {
-                out[(size_t)((p >> 1) * NWARP) * (bz + 2) + 32 * (p & 1)] = v[p];
-                if (RES) worst = fmax(worst, fabs(__dsub_rn(v[p], xm[p])));
-            }
-        }
+        relax_plane<RES, BOX_Z>(reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
+                                reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE), soff,
+                                BOX_Z, BOX_Z, xm, x0, out, bz, live, worst);
         out += plane;
         __syncthreads();  // all warps are done with stage s_c (plane q)
         if (threadIdx.x == 0) {
@@ -237,6 +260,121 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
                                 &bar[s_c]);
             }
         }
+        s_c = s_n;
+    }
+    if (RES) warp_max_to_global(worst, res);
+}
+
+// --------------------------------------------- row-bulk-copy pipeline ----
+// The TMA kernel's schedule, ring and register marching for row pitches a
+// tensor map cannot describe (bz+2 doubles, not a multiple of 16 bytes: odd
+// bz). Each plane tile is staged row by row with non-tensor bulk copies
+// (cp.async.bulk, the same TMA engine and mbarrier transaction counts):
+// a row's 66 doubles start 8 bytes past a 16-byte boundary when its global
+// index is odd, so each row is fetched from the aligned element below it
+// and lands one slot to the right (shift 0/1 per row). With an odd pitch
+// the shift alternates row by row (and plane by plane when the plane size
+// is odd too); a thread's cells all sit on rows of one parity, so it needs
+// one centre shift per plane and y offsets of pitch -+ 1.
+// Measured 0.64 of the HBM roofline at 1536^2 x 1535 (the generic kernel:
+// 0.58): 34 row copies per plane and CTA keep the TMA engine's request rate,
+// not DRAM, the limit; even bz takes the one-request 3-D tensor path (0.99).
+constexpr int RPITCH = TZ + 4;  // 68 doubles = 544 B: every staged row starts 16-byte aligned
+
+template <bool RES>
+__global__ void __launch_bounds__(THREADS, MIN_CTAS)
+stencil_rows_kernel(const double *__restrict__ cur, double *__restrict__ nxt, int bx, int by,
+                    int bz, int i0, int i1, int j0, int j1, int k0, int k1, int ntj, int ntk,
+                    int chunk, int nchunks, int grows, unsigned long long *res) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
+    const Item it = work_item(j0, k0, i0, i1, ntj, ntk, chunk, nchunks, grows);
+    const int jb = it.jb, kb = it.kb, ib = it.ib, nplanes = it.nplanes;
+    const long long pz = (long long)bz + 2, plane = (long long)(by + 2) * pz;
+    const long long total = (long long)(bx + 2) * plane;  // elements in the array
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // tile columns kb-1 .. kb+TZ that exist in a row
+    const int ncols = min(TZ + 2, bz + 2 - (kb - 1));
+
+    // warp 0 stages a plane: lane l copies tile rows l and l+32
+    auto stage_plane = [&](int p, int stage) {
+        const long long g0 = (long long)(ib - 1 + p) * plane + (long long)(jb - 1) * pz + (kb - 1);
+        unsigned bytes[2] = {0, 0};
+        long long from[2] = {0, 0};
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int r = lane + 32 * h;
+            if (r < BOX_Y && jb - 1 + r <= by + 1) {
+                const long long gs = g0 + r * pz;
+                const long long a = gs & ~1LL;
+                long long e = (gs + ncols + 1) & ~1LL;
+                if (e > total) e -= 2;  // only the array's last (unused ghost corner) element
+                from[h] = a;
+                bytes[h] = (unsigned)(e - a) * (unsigned)sizeof(double);
+            }
+        }
+        const unsigned sum = __reduce_add_sync(0xffffffffu, bytes[0] + bytes[1]);
+        if (lane == 0) hx::mbar_expect_tx(&bar[stage], sum);
+        __syncwarp();
+        double *dst = reinterpret_cast<double *>(smem + stage * STAGE_STRIDE);
+#pragma unroll
+        for (int h = 0; h < 2; ++h)
+            if (bytes[h]) hx::bulk_load(dst + (lane + 32 * h) * RPITCH, cur + from[h], bytes[h], &bar[stage]);
+    };
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NSTAGE; ++s) hx::mbar_init(&bar[s], 1);
+        hx::fence_mbar_init();
+    }
+    __syncthreads();
+    if (warp == 0)
+        for (int p = 0; p < NSTAGE && p < nplanes; ++p) stage_plane(p, p);
+
+    // centre shift of this thread's rows (jb + warp + 8m all share a parity)
+    const int s0 = (int)(((long long)(ib - 1) * plane + (long long)(jb + warp) * pz + (kb - 1)) & 1);
+    const int pflip = (int)(plane & 1);  // shifts alternate plane by plane
+    const int podd = (int)(pz & 1);      // ... and row by row
+    auto shift = [&](int p) { return s0 ^ (pflip & p); };
+    auto yoff = [&](int sh) { return podd ? 1 - 2 * sh : 0; };  // neighbour rows' shift - ours
+
+    const int soff = (warp + 1) * RPITCH + lane + 1;
+    double *out = nxt + ((size_t)ib * (by + 2) + (jb + warp)) * (size_t)pz + kb + lane;
+    unsigned live = 0;
+#pragma unroll
+    for (int p = 0; p < PTS; ++p) {
+        const int r = warp + (p >> 1) * NWARP, kk = lane + 32 * (p & 1);
+        if (jb + r < j1 && kb + kk < k1) live |= 1u << p;
+    }
+    double xm[PTS], x0[PTS];
+    double worst = 0.0;
+    int nan_seen = 0;
+    {
+        const double *s0p = reinterpret_cast<const double *>(smem) + shift(0);
+        const double *s1p = reinterpret_cast<const double *>(smem + STAGE_STRIDE) + shift(1);
+        hx::mbar_wait(&bar[0], 0);
+        hx::mbar_wait(&bar[1], 0);
+#pragma unroll
+        for (int p = 0; p < PTS; ++p) {
+            const int o = soff + (p >> 1) * NWARP * RPITCH + 32 * (p & 1);
+            xm[p] = s0p[o];
+            x0[p] = s1p[o];
+            nan_seen |= (xm[p] != xm[p]) | (x0[p] != x0[p]);
+        }
+    }
+    (void)__syncthreads_or(nan_seen);  // consume before stage 0 is refilled (see the TMA kernel)
+    if (warp == 0 && NSTAGE < nplanes) stage_plane(NSTAGE, 0);
+    int s_c = 1;
+    for (int q = 1; q <= nplanes - 2; ++q) {
+        const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;
+        hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
+        const int sq = shift(q), d = yoff(sq);
+        relax_plane<RES, RPITCH>(reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE) + sq,
+                                 reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE) +
+                                     shift(q + 1),
+                                 soff, RPITCH - d, RPITCH + d, xm, x0, out, bz, live, worst);
+        out += plane;
+        __syncthreads();  // all warps are done with stage s_c (plane q)
+        if (warp == 0 && q + NSTAGE < nplanes) stage_plane(q + NSTAGE, s_c);
         s_c = s_n;
     }
     if (RES) warp_max_to_global(worst, res);
@@ -466,6 +604,38 @@ int launch_tma_t(const CUtensorMap &map, double *nxt, int by, int bz, int i0, in
     return 0;
 }
 
+// Tile / chunk / group schedule shared by the TMA and row-bulk-copy pipelines.
+struct Schedule {
+    int ntj, ntk, chunk, nchunks, grows;
+    long items;
+};
+
+Schedule make_schedule(int i0, int i1, int j0, int j1, int k0, int k1) {
+    Schedule sc;
+    const int ni = i1 - i0, nj = j1 - j0, nk = k1 - k0;
+    sc.ntj = (nj + TY - 1) / TY;
+    sc.ntk = (nk + TZ - 1) / TZ;
+    int chunk = g_chunk;
+    if (chunk <= 0) {
+        // Short chunks keep neighbouring CTAs in step (their tile halos are
+        // L2 hits); the grouped order makes the 2 boundary planes a chunk
+        // shares with the next one L2 hits too.
+        // Tuned on B200 at 1536^3 (tools/prof_stencil.py sweeps, profiles/):
+        // chunk 4 with ~288-tile groups reaches ~99% of the measured copy
+        // bandwidth; chunk 10 / ungrouped was 87%, chunk 96 70%.
+        const char *e = getenv("HX_STENCIL_CHUNK");
+        chunk = e ? atoi(e) : 4;
+        if (chunk <= 0) chunk = 4;
+    }
+    sc.chunk = std::min(chunk, ni);
+    sc.nchunks = (ni + sc.chunk - 1) / sc.chunk;
+    int grows = std::max(1, (288 + sc.ntk / 2) / sc.ntk);  // tile rows per scheduling group
+    if (const char *e = getenv("HX_STENCIL_GROUP")) grows = std::max(1, atoi(e));
+    sc.grows = std::min(grows, sc.ntj);
+    sc.items = (long)sc.ntj * sc.ntk * sc.nchunks;
+    return sc;
+}
+
 int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
                int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
     // every tile starts at kb = k0 + t*TZ (TZ even): one box width per launch
@@ -474,36 +644,49 @@ int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, i
     CUtensorMap map;
     int rc = tensor_map_for(cur, bx, by, bz, box_z, &map);
     if (rc) return rc;
-    const int ni = i1 - i0, nj = j1 - j0, nk = k1 - k0;
-    const int ntj = (nj + TY - 1) / TY, ntk = (nk + TZ - 1) / TZ;
-    int chunk = g_chunk;
-    if (chunk <= 0) {
-        // Short chunks keep neighbouring CTAs in step (their tile halos are
-        // L2 hits); the grouped order below makes the 2 boundary planes a
-        // chunk shares with the next one L2 hits too.
-        // Tuned on B200 at 1536^3 (tools/prof_stencil.py sweeps, profiles/):
-        // chunk 4 with ~288-tile groups reaches ~99% of the measured copy
-        // bandwidth; chunk 10 / ungrouped was 87%, chunk 96 70%.
-        const char *e = getenv("HX_STENCIL_CHUNK");
-        chunk = e ? atoi(e) : 4;
-        if (chunk <= 0) chunk = 4;
-    }
-    chunk = std::min(chunk, ni);
-    const int nchunks = (ni + chunk - 1) / chunk;
-    int grows = std::max(1, (288 + ntk / 2) / ntk);  // tile rows per scheduling group
-    if (const char *e = getenv("HX_STENCIL_GROUP")) grows = std::max(1, atoi(e));
-    grows = std::min(grows, ntj);
-    const long items = (long)ntj * ntk * nchunks;
-    if (items > 0x7fffffffL) return HX_E_INVALID;
+    const Schedule sc = make_schedule(i0, i1, j0, j1, k0, k1);
+    if (sc.items > 0x7fffffffL) return HX_E_INVALID;
     if (shifted)
-        return res ? launch_tma_t<true, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
-                                                chunk, nchunks, grows, items, res, st)
-                   : launch_tma_t<false, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
-                                                 chunk, nchunks, grows, items, res, st);
-    return res ? launch_tma_t<true, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
-                                            chunk, nchunks, grows, items, res, st)
-               : launch_tma_t<false, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk,
-                                             chunk, nchunks, grows, items, res, st);
+        return res ? launch_tma_t<true, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj,
+                                                sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
+                   : launch_tma_t<false, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj,
+                                                 sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
+    return res ? launch_tma_t<true, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk,
+                                            sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
+               : launch_tma_t<false, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk,
+                                             sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
+}
+
+template <bool RES>
+int launch_rows_t(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
+                  int j1, int k0, int k1, const Schedule &sc, unsigned long long *res,
+                  cudaStream_t st) {
+    static unsigned long long attr_set = 0;  // per device, as for the TMA kernel
+    int dev = 0;
+    HX_TRY(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(attr_set & bit)) {
+        HX_TRY(cudaFuncSetAttribute(stencil_rows_kernel<RES>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
+        HX_TRY(cudaFuncSetAttribute(stencil_rows_kernel<RES>,
+                                    cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared));
+        attr_set |= bit;
+    }
+    stencil_rows_kernel<RES><<<(unsigned)sc.items, THREADS, SMEM_BYTES, st>>>(
+        cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk, sc.chunk, sc.nchunks,
+        sc.grows, res);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
+int launch_rows(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
+                int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
+    if (((uintptr_t)cur & 15) != 0) return HX_E_INVALID;  // bulk copies need a 16-byte base
+    const Schedule sc = make_schedule(i0, i1, j0, j1, k0, k1);
+    if (sc.items > 0x7fffffffL) return HX_E_INVALID;
+    return res ? launch_rows_t<true>(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, sc, res, st)
+               : launch_rows_t<false>(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, sc, res, st);
 }
 
 // Thin boundary slabs of the overlap split (one plane / row / column thick):
@@ -642,7 +825,7 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
         const int ka = ((k0 - 1) & 1) ? k0 - 2 : k0 - 1;
         const bool zcol = k1 - k0 == 1 && (j1 - j0) >= 32 && tma_eligible(cur, bz) &&
                           ka >= 0 && ka + 3 <= bz + 1;
-        want = zcol ? 4 : thin ? 3 : (tma_eligible(cur, bz) ? 1 : 2);
+        want = zcol ? 4 : thin ? 3 : (tma_eligible(cur, bz) ? 1 : 5);
     }
     if (want == 4) {
         const int ka = ((k0 - 1) & 1) ? k0 - 2 : k0 - 1;
@@ -654,6 +837,10 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
         g_last_variant = 3;
         return launch_slab(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);
     }
+    if (want == 5 || (want == 1 && !tma_eligible(cur, bz) && g_variant == 0)) {
+        g_last_variant = 5;
+        return launch_rows(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
+    }
     if (want == 1 && !tma_eligible(cur, bz)) return HX_E_INVALID;
     if (want == 1) {
         int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
@@ -662,6 +849,8 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
             return 0;
         }
         if (g_variant == 1) return rc;  // forced: report, do not fall back
+        g_last_variant = 5;             // no tensor map (driver entry point): same pipeline
+        return launch_rows(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
     }
     g_last_variant = 2;
     return launch_generic(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);

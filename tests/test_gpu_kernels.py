@@ -62,7 +62,7 @@ def run_stencil(hx, cur, variant, res=False, box=None):
 
 
 @pytest.mark.parametrize("shape", SHAPES)
-@pytest.mark.parametrize("variant", [0, 2, 3])
+@pytest.mark.parametrize("variant", [0, 2, 3, 5])
 def test_stencil_bitexact_vs_oracle(hx, shape, variant):
     rng = np.random.default_rng(sum(shape))
     cur = rng.standard_normal(tuple(s + 2 for s in shape))
@@ -73,8 +73,9 @@ def test_stencil_bitexact_vs_oracle(hx, shape, variant):
     assert res == wres
     if variant == 0:
         thin = shape[1] < 8 or shape[2] < 16
-        expect = 3 if thin else (1 if (shape[2] + 2) % 2 == 0 else 2)
-        assert hx.raw("hx_stencil_last_variant")() == expect  # TMA for every thick even-z box
+        expect = 3 if thin else (1 if (shape[2] + 2) % 2 == 0 else 5)
+        # TMA for every thick even-z box, the row-bulk-copy pipeline for odd z
+        assert hx.raw("hx_stencil_last_variant")() == expect
 
 
 def test_div6_matches_correctly_rounded_division(hx):
@@ -122,7 +123,7 @@ def test_tma_chunking_is_invisible(hx, chunk):
     assert got.tobytes() == want.tobytes()
 
 
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 5])
 def test_box_plus_shells_equal_full_sweep(hx, variant):
     """Interior box + six boundary slabs (the overlap split) == one sweep."""
     rng = np.random.default_rng(11)
@@ -325,3 +326,44 @@ def test_residual_monotone_after_ten_iterations(hx):
     _, res = sequential_oracle((64, 64, 64), 60)
     assert all(np.isfinite(res)) and res[0] > 0
     assert all(b <= a for a, b in zip(res[10:], res[11:]))
+
+
+@pytest.mark.parametrize("shape", [(40, 70, 129), (17, 65, 63), (5, 33, 1), (64, 64, 64), (9, 31, 33),
+                                   (3, 2, 65)])
+@pytest.mark.parametrize("chunk", [0, 1, 5])
+def test_row_pipeline_odd_z_and_chunks(hx, shape, chunk):
+    """Variant 5 (rows staged by bulk copies with per-row alignment shifts,
+    the TMA kernel's schedule) on odd row pitches and odd plane sizes,
+    partial tiles and chunkings, with the residual."""
+    rng = np.random.default_rng(sum(shape) + chunk)
+    cur = rng.standard_normal(tuple(s + 2 for s in shape))
+    hx.raw("hx_stencil_set_chunk")(chunk)
+    try:
+        nxt0, got, res = run_stencil(hx, cur, 5, res=True)
+    finally:
+        hx.raw("hx_stencil_set_chunk")(0)
+    want = nxt0.copy()
+    assert res == jacobi_c.stencil_residual(cur, want)
+    assert got.tobytes() == want.tobytes()
+
+
+def test_row_pipeline_odd_z_sub_boxes(hx):
+    """Interior box + shells of an odd-z block through the auto selection
+    (row-bulk-copy interior) equal one sweep."""
+    rng = np.random.default_rng(21)
+    bx, by, bz = 20, 40, 67
+    cur = rng.standard_normal((bx + 2, by + 2, bz + 2))
+    boxes = [(2, bx, 2, by, 2, bz), (1, 2, 1, by + 1, 1, bz + 1), (bx, bx + 1, 1, by + 1, 1, bz + 1),
+             (2, bx, 1, 2, 1, bz + 1), (2, bx, by, by + 1, 1, bz + 1), (2, bx, 2, by, 1, 2),
+             (2, bx, 2, by, bz, bz + 1)]
+    c = dev(cur)
+    nxt0 = rng.standard_normal(cur.shape)
+    n = dev(nxt0)
+    hx.raw("hx_stencil_set_variant")(0)
+    for box in boxes:
+        hx.call("hx_stencil_box", c.data_ptr(), n.data_ptr(), bx, by, bz, *box, None, stream())
+        if box is boxes[0]:
+            assert hx.raw("hx_stencil_last_variant")() == 5
+    want = nxt0.copy()
+    jacobi_np.stencil(cur, want)
+    assert n.cpu().numpy().tobytes() == want.tobytes()
