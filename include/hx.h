@@ -111,9 +111,10 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz,
  * (auto when the padded row pitch is a multiple of 16 bytes, i.e. even bz),
  * 2 generic, 3 flattened slab (auto for boxes thinner than 8 rows or 16
  * columns — the overlap split's boundary shell), 4 single z column with
- * aligned quad loads (auto for one-column boxes), 5 row-bulk-copy pipeline
- * (the TMA kernel's schedule, rows staged by non-tensor bulk copies; auto
- * for odd bz, whose row pitch a tensor map cannot describe).
+ * aligned quad loads (auto for one-column boxes), 5 row-pair TMA pipeline
+ * (the TMA kernel through four parity-class tensor maps with 2-row / 2-plane
+ * strides; auto for odd bz, whose row pitch a plain tensor map cannot
+ * describe).
  * Returns the previous one. */
 int hx_stencil_set_variant(int variant);
 int hx_stencil_last_variant(void);

@@ -116,9 +116,9 @@ __device__ __forceinline__ void warp_max_to_global(double worst, unsigned long l
 // One x plane of a tile from two staged planes: P0 holds plane q (y/z
 // neighbours), PP plane q+1; xm/x0 carry planes q-1 and q in registers and
 // are advanced. Stores the live cells of plane q and folds their residual.
-// ylo / yhi: distance from a cell to its y-1 / y+1 neighbour in P0 (the row
-// pitch, or pitch -+ 1 when rows are staged with alternating alignment).
-template <bool RES, int BOX_Z>
+// ROWSTEP: staged distance between a thread's rows r and r + NWARP; ylo /
+// yhi: distance from a cell to its y-1 / y+1 neighbour in P0.
+template <bool RES, int ROWSTEP>
 __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, int soff, int ylo,
                                             int yhi, double (&xm)[PTS], double (&x0)[PTS],
                                             double *out, int bz, unsigned live, double &worst) {
@@ -126,7 +126,7 @@ __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, 
     bool fast = true;
 #pragma unroll
     for (int p = 0; p < PTS; ++p) {
-        const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
+        const int o = soff + (p >> 1) * ROWSTEP + 32 * (p & 1);
         const double xp = PP[o];
         v[p] = sum6(xm[p], xp, P0[o - ylo], P0[o + yhi], P0[o - 1], P0[o + 1]);
         xm[p] = x0[p];
@@ -247,7 +247,7 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     for (int q = 1; q <= nplanes - 2; ++q) {
         const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;  // stage holding plane q+1
         hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
-        relax_plane<RES, BOX_Z>(reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
+        relax_plane<RES, NWARP * BOX_Z>(reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
                                 reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE), soff,
                                 BOX_Z, BOX_Z, xm, x0, out, bz, live, worst);
         out += plane;
@@ -265,79 +265,77 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     if (RES) warp_max_to_global(worst, res);
 }
 
-// --------------------------------------------- row-bulk-copy pipeline ----
-// The TMA kernel's schedule, ring and register marching for row pitches a
-// tensor map cannot describe (bz+2 doubles, not a multiple of 16 bytes: odd
-// bz). Each plane tile is staged row by row with non-tensor bulk copies
-// (cp.async.bulk, the same TMA engine and mbarrier transaction counts):
-// a row's 66 doubles start 8 bytes past a 16-byte boundary when its global
-// index is odd, so each row is fetched from the aligned element below it
-// and lands one slot to the right (shift 0/1 per row). With an odd pitch
-// the shift alternates row by row (and plane by plane when the plane size
-// is odd too); a thread's cells all sit on rows of one parity, so it needs
-// one centre shift per plane and y offsets of pitch -+ 1.
-// Measured 0.64 of the HBM roofline at 1536^2 x 1535 (the generic kernel:
-// 0.58): 34 row copies per plane and CTA keep the TMA engine's request rate,
-// not DRAM, the limit; even bz takes the one-request 3-D tensor path (0.99).
-constexpr int RPITCH = TZ + 4;  // 68 doubles = 544 B: every staged row starts 16-byte aligned
+// ------------------------------------------- row-pair tensor pipeline ----
+// The TMA kernel for row pitches a plain 3-D tensor map cannot describe
+// (bz + 2 doubles, not a multiple of 16 bytes: odd bz). The array is viewed
+// through four tensor maps, one per (row parity a, plane parity b) class:
+//   element (i, j, k) = base + (i>>1) 2 plane + (j>>1) 2 pz + [k + a pz + b plane]
+// with strides 2 pz and 2 plane doubles (16-byte multiples for any parity)
+// and the bracket as the dim-0 coordinate (dim-0 extent a pz + b plane + pz,
+// so past-the-row columns read as out-of-bounds zeros, never past the array).
+// Every row of a class starts with the same alignment, so one box per class
+// (17 rows x 68 doubles, started one element early when the row start is
+// odd) stages the tile's even or odd rows: two tensor loads per plane.
+// Measured (tools/prof_stencil.py): 1536^2 x 1535 at 0.999 and 1535^3 at
+// 0.997 of the HBM roofline (the generic kernel: 0.58; staging rows with
+// 34 separate bulk copies per plane: 0.64, TMA-request bound).
+constexpr int PW = TZ + 4;   // box width in doubles (66 needed + alignment shift, 544 B)
+constexpr int PH = BOX_Y / 2;  // 17 rows per parity box
+constexpr int PREG = (PH * PW * (int)sizeof(double) + 127) / 128 * 128 / (int)sizeof(double);
+constexpr unsigned PSTAGE = 2 * PREG * sizeof(double);
+constexpr size_t PSMEM_BYTES = (size_t)NSTAGE * PSTAGE + NSTAGE * sizeof(uint64_t);
+
+struct PairMaps {
+    CUtensorMap m[4];  // index a + 2 b
+};
 
 template <bool RES>
 __global__ void __launch_bounds__(THREADS, MIN_CTAS)
-stencil_rows_kernel(const double *__restrict__ cur, double *__restrict__ nxt, int bx, int by,
-                    int bz, int i0, int i1, int j0, int j1, int k0, int k1, int ntj, int ntk,
-                    int chunk, int nchunks, int grows, unsigned long long *res) {
+stencil_pair_kernel(const __grid_constant__ PairMaps maps, double *__restrict__ nxt, int by, int bz,
+                    int i0, int i1, int j0, int j1, int k0, int k1, int ntj, int ntk, int chunk,
+                    int nchunks, int grows, unsigned long long *res) {
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * PSTAGE);
     const Item it = work_item(j0, k0, i0, i1, ntj, ntk, chunk, nchunks, grows);
     const int jb = it.jb, kb = it.kb, ib = it.ib, nplanes = it.nplanes;
     const long long pz = (long long)bz + 2, plane = (long long)(by + 2) * pz;
-    const long long total = (long long)(bx + 2) * plane;  // elements in the array
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    // tile columns kb-1 .. kb+TZ that exist in a row
-    const int ncols = min(TZ + 2, bz + 2 - (kb - 1));
-
-    // warp 0 stages a plane: lane l copies tile rows l and l+32
-    auto stage_plane = [&](int p, int stage) {
-        const long long g0 = (long long)(ib - 1 + p) * plane + (long long)(jb - 1) * pz + (kb - 1);
-        unsigned bytes[2] = {0, 0};
-        long long from[2] = {0, 0};
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int r = lane + 32 * h;
-            if (r < BOX_Y && jb - 1 + r <= by + 1) {
-                const long long gs = g0 + r * pz;
-                const long long a = gs & ~1LL;
-                long long e = (gs + ncols + 1) & ~1LL;
-                if (e > total) e -= 2;  // only the array's last (unused ghost corner) element
-                from[h] = a;
-                bytes[h] = (unsigned)(e - a) * (unsigned)sizeof(double);
-            }
-        }
-        const unsigned sum = __reduce_add_sync(0xffffffffu, bytes[0] + bytes[1]);
-        if (lane == 0) hx::mbar_expect_tx(&bar[stage], sum);
-        __syncwarp();
-        double *dst = reinterpret_cast<double *>(smem + stage * STAGE_STRIDE);
-#pragma unroll
-        for (int h = 0; h < 2; ++h)
-            if (bytes[h]) hx::bulk_load(dst + (lane + 32 * h) * RPITCH, cur + from[h], bytes[h], &bar[stage]);
+    // local row parity l (tile row R = l + 2m) -> global row class a_l
+    const int a0 = (jb - 1) & 1, a1 = jb & 1;
+    // staging shift of local-parity region l at padded plane P
+    auto shift = [&](int l, int P) {
+        return (int)(((long long)(kb - 1) + (l ? a1 : a0) * pz + (P & 1) * plane) & 1);
     };
-
+    auto load_plane = [&](int p, int stage) {  // thread 0: both parity boxes of plane ib-1+p
+        const int P = ib - 1 + p;
+        hx::mbar_expect_tx(&bar[stage], (unsigned)(2 * PH * PW * sizeof(double)));
+#pragma unroll
+        for (int l = 0; l < 2; ++l) {
+            const int a = l ? a1 : a0;
+            const int c0 = (kb - 1) + (int)(a * pz + (P & 1) * plane) - shift(l, P);
+            hx::tma_load_3d(smem + stage * PSTAGE + l * PREG * sizeof(double), &maps.m[a + 2 * (P & 1)],
+                            c0, (jb - 1 + l) >> 1, P >> 1, &bar[stage]);
+        }
+    };
     if (threadIdx.x == 0) {
-        for (int s = 0; s < NSTAGE; ++s) hx::mbar_init(&bar[s], 1);
+        for (int q = 0; q < 4; ++q) hx::prefetch_tmap(&maps.m[q]);
+        for (int q = 0; q < NSTAGE; ++q) hx::mbar_init(&bar[q], 1);
         hx::fence_mbar_init();
+        for (int p = 0; p < NSTAGE && p < nplanes; ++p) load_plane(p, p);
     }
     __syncthreads();
-    if (warp == 0)
-        for (int p = 0; p < NSTAGE && p < nplanes; ++p) stage_plane(p, p);
 
-    // centre shift of this thread's rows (jb + warp + 8m all share a parity)
-    const int s0 = (int)(((long long)(ib - 1) * plane + (long long)(jb + warp) * pz + (kb - 1)) & 1);
-    const int pflip = (int)(plane & 1);  // shifts alternate plane by plane
-    const int podd = (int)(pz & 1);      // ... and row by row
-    auto shift = [&](int p) { return s0 ^ (pflip & p); };
-    auto yoff = [&](int sh) { return podd ? 1 - 2 * sh : 0; };  // neighbour rows' shift - ours
-
-    const int soff = (warp + 1) * RPITCH + lane + 1;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    // this thread's rows R = warp + 1 + 8m sit in region rc at row (R >> 1);
+    // their y-1 / y+1 neighbours in the other region
+    const int rc = (warp + 1) & 1;
+    const int c_row = (warp + 1) >> 1, lo_row = warp >> 1, hi_row = (warp + 2) >> 1;
+    const int soff = rc * PREG + c_row * PW + lane + 1;
+    auto ylo = [&](int P) {
+        return soff - ((1 - rc) * PREG + lo_row * PW + lane + 1) + shift(rc, P) - shift(1 - rc, P);
+    };
+    auto yhi = [&](int P) {
+        return ((1 - rc) * PREG + hi_row * PW + lane + 1) - soff + shift(1 - rc, P) - shift(rc, P);
+    };
     double *out = nxt + ((size_t)ib * (by + 2) + (jb + warp)) * (size_t)pz + kb + lane;
     unsigned live = 0;
 #pragma unroll
@@ -349,32 +347,32 @@ stencil_rows_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
     double worst = 0.0;
     int nan_seen = 0;
     {
-        const double *s0p = reinterpret_cast<const double *>(smem) + shift(0);
-        const double *s1p = reinterpret_cast<const double *>(smem + STAGE_STRIDE) + shift(1);
+        const double *s0 = reinterpret_cast<const double *>(smem) + shift(rc, ib - 1);
+        const double *s1 = reinterpret_cast<const double *>(smem + PSTAGE) + shift(rc, ib);
         hx::mbar_wait(&bar[0], 0);
         hx::mbar_wait(&bar[1], 0);
 #pragma unroll
         for (int p = 0; p < PTS; ++p) {
-            const int o = soff + (p >> 1) * NWARP * RPITCH + 32 * (p & 1);
-            xm[p] = s0p[o];
-            x0[p] = s1p[o];
+            const int o = soff + (p >> 1) * (NWARP / 2) * PW + 32 * (p & 1);
+            xm[p] = s0[o];
+            x0[p] = s1[o];
             nan_seen |= (xm[p] != xm[p]) | (x0[p] != x0[p]);
         }
     }
     (void)__syncthreads_or(nan_seen);  // consume before stage 0 is refilled (see the TMA kernel)
-    if (warp == 0 && NSTAGE < nplanes) stage_plane(NSTAGE, 0);
+    if (threadIdx.x == 0 && NSTAGE < nplanes) load_plane(NSTAGE, 0);
     int s_c = 1;
     for (int q = 1; q <= nplanes - 2; ++q) {
         const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;
         hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
-        const int sq = shift(q), d = yoff(sq);
-        relax_plane<RES, RPITCH>(reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE) + sq,
-                                 reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE) +
-                                     shift(q + 1),
-                                 soff, RPITCH - d, RPITCH + d, xm, x0, out, bz, live, worst);
+        const int P = ib - 1 + q;
+        relax_plane<RES, (NWARP / 2) * PW>(
+            reinterpret_cast<const double *>(smem + s_c * PSTAGE) + shift(rc, P),
+            reinterpret_cast<const double *>(smem + s_n * PSTAGE) + shift(rc, P + 1), soff, ylo(P),
+            yhi(P), xm, x0, out, bz, live, worst);
         out += plane;
         __syncthreads();  // all warps are done with stage s_c (plane q)
-        if (warp == 0 && q + NSTAGE < nplanes) stage_plane(q + NSTAGE, s_c);
+        if (threadIdx.x == 0 && q + NSTAGE < nplanes) load_plane(q + NSTAGE, s_c);
         s_c = s_n;
     }
     if (RES) warp_max_to_global(worst, res);
@@ -657,36 +655,78 @@ int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, i
                                              sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
 }
 
+// The four (row parity, plane parity) class maps of stencil_pair_kernel.
+std::map<std::tuple<const void *, int, int, int, int>, PairMaps> g_pair_maps;
+
+int pair_maps_for(const double *cur, int bx, int by, int bz, PairMaps *out) {
+    const int promo = l2_promotion();
+    auto key = std::make_tuple((const void *)cur, bx, by, bz, promo);
+    {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        auto it = g_pair_maps.find(key);
+        if (it != g_pair_maps.end()) {
+            *out = it->second;
+            return 0;
+        }
+    }
+    auto encode = (PFN_cuTensorMapEncodeTiled_v12000)hx_internal_driver_sym("cuTensorMapEncodeTiled");
+    if (!encode) return HX_E_NODRIVER;
+    const cuuint64_t pz = (cuuint64_t)bz + 2, py = (cuuint64_t)by + 2, px = (cuuint64_t)bx + 2;
+    const cuuint64_t plane = py * pz;
+    PairMaps pm;
+    for (int b = 0; b < 2; ++b)
+        for (int a = 0; a < 2; ++a) {
+            cuuint64_t dims[3] = {a * pz + b * plane + pz, (py - a + 1) / 2, (px - b + 1) / 2};
+            cuuint64_t strides[2] = {2 * pz * sizeof(double), 2 * plane * sizeof(double)};
+            cuuint32_t box[3] = {(cuuint32_t)PW, (cuuint32_t)PH, 1};
+            cuuint32_t estr[3] = {1, 1, 1};
+            CUresult r = encode(&pm.m[a + 2 * b], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)cur,
+                                dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                CU_TENSOR_MAP_SWIZZLE_NONE, (CUtensorMapL2promotion)promo,
+                                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+            if (r != CUDA_SUCCESS) return HX_E_TMA;
+        }
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_pair_maps.size() > 64) g_pair_maps.clear();
+    g_pair_maps[key] = pm;
+    *out = pm;
+    return 0;
+}
+
 template <bool RES>
-int launch_rows_t(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
-                  int j1, int k0, int k1, const Schedule &sc, unsigned long long *res,
-                  cudaStream_t st) {
+int launch_pair_t(const PairMaps &pm, double *nxt, int by, int bz, int i0, int i1, int j0, int j1,
+                  int k0, int k1, const Schedule &sc, unsigned long long *res, cudaStream_t st) {
     static unsigned long long attr_set = 0;  // per device, as for the TMA kernel
     int dev = 0;
     HX_TRY(cudaGetDevice(&dev));
     const unsigned long long bit = 1ull << (dev & 63);
     if (!(attr_set & bit)) {
-        HX_TRY(cudaFuncSetAttribute(stencil_rows_kernel<RES>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-        HX_TRY(cudaFuncSetAttribute(stencil_rows_kernel<RES>,
+        HX_TRY(cudaFuncSetAttribute(stencil_pair_kernel<RES>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSMEM_BYTES));
+        HX_TRY(cudaFuncSetAttribute(stencil_pair_kernel<RES>,
                                     cudaFuncAttributePreferredSharedMemoryCarveout,
                                     (int)cudaSharedmemCarveoutMaxShared));
         attr_set |= bit;
     }
-    stencil_rows_kernel<RES><<<(unsigned)sc.items, THREADS, SMEM_BYTES, st>>>(
-        cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk, sc.chunk, sc.nchunks,
-        sc.grows, res);
+    stencil_pair_kernel<RES><<<(unsigned)sc.items, THREADS, PSMEM_BYTES, st>>>(
+        pm, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk, sc.chunk, sc.nchunks, sc.grows,
+        res);
     HX_LAUNCH_CHECK();
     return 0;
 }
 
-int launch_rows(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
+int launch_pair(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
                 int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
-    if (((uintptr_t)cur & 15) != 0) return HX_E_INVALID;  // bulk copies need a 16-byte base
+    if (((uintptr_t)cur & 15) != 0) return HX_E_INVALID;  // tensor maps need a 16-byte base
+    const long long plane = (long long)(by + 2) * (bz + 2);
+    if (plane + 2LL * (bz + 2) + PW >= 0x7fffffffLL) return HX_E_INVALID;  // int box coordinates
+    PairMaps pm;
+    int rc = pair_maps_for(cur, bx, by, bz, &pm);
+    if (rc) return rc;
     const Schedule sc = make_schedule(i0, i1, j0, j1, k0, k1);
     if (sc.items > 0x7fffffffL) return HX_E_INVALID;
-    return res ? launch_rows_t<true>(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, sc, res, st)
-               : launch_rows_t<false>(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, sc, res, st);
+    return res ? launch_pair_t<true>(pm, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc, res, st)
+               : launch_pair_t<false>(pm, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc, res, st);
 }
 
 // Thin boundary slabs of the overlap split (one plane / row / column thick):
@@ -839,7 +879,7 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
     }
     if (want == 5 || (want == 1 && !tma_eligible(cur, bz) && g_variant == 0)) {
         g_last_variant = 5;
-        return launch_rows(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
+        return launch_pair(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
     }
     if (want == 1 && !tma_eligible(cur, bz)) return HX_E_INVALID;
     if (want == 1) {
@@ -850,7 +890,7 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
         }
         if (g_variant == 1) return rc;  // forced: report, do not fall back
         g_last_variant = 5;             // no tensor map (driver entry point): same pipeline
-        return launch_rows(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
+        return launch_pair(cur, nxt, bx, by, bz, i0, i1, j0, j1, k0, k1, res, st);
     }
     g_last_variant = 2;
     return launch_generic(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);

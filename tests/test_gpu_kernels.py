@@ -74,7 +74,7 @@ def test_stencil_bitexact_vs_oracle(hx, shape, variant):
     if variant == 0:
         thin = shape[1] < 8 or shape[2] < 16
         expect = 3 if thin else (1 if (shape[2] + 2) % 2 == 0 else 5)
-        # TMA for every thick even-z box, the row-bulk-copy pipeline for odd z
+        # TMA for every thick even-z box, the row-pair TMA pipeline for odd z
         assert hx.raw("hx_stencil_last_variant")() == expect
 
 
@@ -332,9 +332,9 @@ def test_residual_monotone_after_ten_iterations(hx):
                                    (3, 2, 65)])
 @pytest.mark.parametrize("chunk", [0, 1, 5])
 def test_row_pipeline_odd_z_and_chunks(hx, shape, chunk):
-    """Variant 5 (rows staged by bulk copies with per-row alignment shifts,
-    the TMA kernel's schedule) on odd row pitches and odd plane sizes,
-    partial tiles and chunkings, with the residual."""
+    """Variant 5 (parity-class tensor maps: even and odd rows staged by two
+    boxes with their own alignment shifts) on odd row pitches and odd plane
+    sizes, partial tiles and chunkings, with the residual."""
     rng = np.random.default_rng(sum(shape) + chunk)
     cur = rng.standard_normal(tuple(s + 2 for s in shape))
     hx.raw("hx_stencil_set_chunk")(chunk)
@@ -349,7 +349,7 @@ def test_row_pipeline_odd_z_and_chunks(hx, shape, chunk):
 
 def test_row_pipeline_odd_z_sub_boxes(hx):
     """Interior box + shells of an odd-z block through the auto selection
-    (row-bulk-copy interior) equal one sweep."""
+    (row-pair TMA interior) equal one sweep."""
     rng = np.random.default_rng(21)
     bx, by, bz = 20, 40, 67
     cur = rng.standard_normal((bx + 2, by + 2, bz + 2))
