@@ -1,33 +1,46 @@
-"""Persistent-channel Jacobi3D engine: one block per GPU, NVLink peer puts.
+"""Persistent-channel Jacobi3D engine: one block per GPU, NVLink peer stores.
 
 This is the B200 form of the paper's Channel API applied to the Jacobi3D
 halo exchange (paper §3.2.2 + §4.3; reference loop cl/jacobi3d.py:246-279,
-channels cl/channels.py:75-99). Each block owns an IPC-exportable receive
-arena in HBM:
+channels cl/channels.py:75-99). Each block owns an IPC-exportable arena in
+HBM,
 
     [flags: 6 x u64][counters: 6 x u32][err: i32][pad][slot[parity][dir] ...]
 
-created once and mapped by its neighbours (CUDA IPC handle cache across
-processes, plain P2P pointers inside one process). Per iteration, on one
-stream per GPU and with no host involvement:
+and its two fields; both are exported once to the neighbours (CUDA IPC
+handle cache across processes, plain P2P pointers inside one process). The
+channel counter is a 64-bit flag value, so no tag or metadata ever crosses
+(paper Fig. 6-7). Two exchanges share that set-up:
 
+exchange="fused" (default). Per iteration it and block, with no host
+involvement:
+  * comm stream: ONE hx_shell_put — every CTA acquires its flags >= it + 1
+    (the neighbours' boundary of it - 1 is in cur's ghost planes, and they
+    have finished reading the ghost planes about to be written), relaxes the
+    boundary shell and stores each neighbour-facing cell both into nxt and
+    over NVLink straight into the neighbour's nxt ghost plane, then the last
+    CTA release-stores flag = it + 2 in every neighbour's arena;
+  * main stream, concurrently: the TMA sweep of the interior box, then a
+    wait for the shell's event.
+  One channel exchange (below) before the first step primes the ghosts.
+
+exchange="p2p" (the channel kernels; overlap=True adds the interior /
+boundary split):
   1. hx_pack_put: pack every neighbour-facing interior plane straight into
-     the neighbour's slot[it & 1][d ^ 1] over NVLink (fused pack + put) and,
-     once all CTAs of that face have stored, release-store flag = it + 1 in
-     the neighbour's arena — the channel counter is the flag value, so no
-     tag or metadata ever crosses (paper Fig. 6-7);
+     the neighbour's slot[it & 1][d ^ 1] over NVLink and, once all CTAs have
+     stored, release-store flag = it + 1 in the neighbour's arena;
   2. hx_wait_unpack: acquire own flags >= it + 1 and unpack the slots into
      the ghost planes;
   3. hx_stencil (TMA pipeline) cur -> nxt, optional fused residual.
+  Two parity slots suffice: a neighbour can run at most one iteration ahead
+  (cl/jacobi3d.py:146) because its put for it + 2 needs our flag for it + 1,
+  which we publish only after unpacking iteration it.
 
-Two parity slots suffice: a neighbour can run at most one iteration ahead
-(cl/jacobi3d.py:146) because its put for it + 2 needs our flag for it + 1,
-which we publish only after unpacking iteration it.
-
-Blocks hosted by the same process (the single-GPU emulation used by the
-tests) are driven on ONE stream in phase order — all puts, then all waits,
-then all stencils — so a wait never precedes the put it depends on and no
-two waiting kernels ever need to be co-resident on a GPU.
+Every device-side wait points at work of an EARLIER launch (another GPU's,
+or one queued before it on the same stream): blocks hosted by one process
+on one GPU share that GPU's streams and are driven in phase order, so no
+kernel ever waits for one launched after it and no two waiting kernels need
+to be co-resident.
 """
 
 from __future__ import annotations
