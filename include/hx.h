@@ -182,6 +182,35 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
                  unsigned int *counter, unsigned long long timeout_ns, int *err,
                  unsigned long long *res, void *stream);
 
+/* --------------------------------------------------- persistent channel --
+ * The Channel API's metadata-free stream (cl/channels.py:33-102; paper
+ * §3.2.2) in its pre-registered device form. One direction is a ring of
+ * `depth` slots (`stride` bytes apart) in the receiver's HBM and a credit
+ * counter on the sender; a slot holds a 16-byte header — tag k+1 in the high
+ * 32 bits and the length in the low 32, i.e. the arrival flag and the length
+ * in one word — then the payload. Payloads up to HX_CHAN_LL_MAX bytes go as
+ * LL words (8-byte stores of 4 data bytes + the tag: no fences, the receiver
+ * polls the data), larger ones as a bulk copy published by a release store
+ * of the header. The message index is device state (*seq, one per endpoint,
+ * advanced by each launch), so send/recv sequences can be captured in CUDA
+ * graphs.
+ *   send k: wait until *credit >= k+1-depth (slot k % depth free), write
+ *           the payload into the slot (a peer-mapped pointer) and its header.
+ *   recv k: wait for the header tag, copy min(len, capacity) bytes into dst,
+ *           write len to *len_out (nullable; len > capacity = truncated) and
+ *           store *credit = k+1 (a peer-mapped pointer).
+ * stride must cover 16 + the payload (16 + 8 * ceil(bytes / 4) for LL).
+ * counter: one zero-initialised uint32 per endpoint and direction. Waits
+ * are bounded by timeout_ns (then *err = HX_E_TIMEOUT). */
+#define HX_CHAN_LL_MAX 8192u
+int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int depth,
+                 unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
+                 unsigned long long timeout_ns, int *err, void *stream);
+int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, int depth,
+                 unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
+                 unsigned long long *len_out, unsigned long long timeout_ns, int *err,
+                 void *stream);
+
 /* ---------------------------------------------------------------- flags --
  * Persistent-channel completion words (the Channel API's per-direction
  * counter, cl/channels.py:75-99, carried as a 64-bit flag value). */

@@ -257,6 +257,155 @@ __device__ __forceinline__ void st_relaxed_sys(unsigned long long *p, unsigned l
     asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// ------------------------------------------------- persistent channel ----
+// One direction of a pre-registered channel (paper §3.2.2): a ring of
+// `depth` slots in the receiver's HBM and a credit counter on the sender.
+// A slot is [header u64][pad][payload]; the header (tag = k + 1 in the high
+// 32 bits, length in the low 32) is both the arrival flag and the length,
+// so one word per message crosses besides the data. Payloads up to
+// HX_CHAN_LL_MAX travel as LL words (4 data bytes + the tag per 8-byte
+// store, like the LL ping-pong): no fence on either side, the receiver polls
+// the data itself. Larger payloads are bulk-copied and published by a
+// release store of the header. The message index lives on the device (seq,
+// advanced by each launch), so launch sequences can be graph-captured.
+struct ChanDir {
+    char *slots;                     // depth x stride, receiver HBM (peer-mapped for send)
+    unsigned long long *credit;      // sender: messages consumed by the receiver
+    unsigned long long *seq;         // this endpoint's message counter (local)
+    unsigned int *counter;           // last-CTA counter (local, zero-initialised)
+    unsigned long long stride;
+    int depth;
+};
+
+constexpr unsigned long long CHAN_HDR = 16;
+
+// True in the CTA that finishes last (after every CTA's copy). A single CTA
+// needs no counter: the barrier orders its threads' stores before thread
+// 0's system-scope release, which is cumulative over them.
+__device__ __forceinline__ bool chan_last_cta(unsigned int *counter) {
+    __shared__ bool last;
+    __syncthreads();
+    if (gridDim.x == 1) return true;
+    if (threadIdx.x == 0) {
+        __threadfence_system();  // this CTA's copy, before the count
+        last = atomicAdd(counter, 1u) + 1u == gridDim.x;
+        if (last) *counter = 0u;
+    }
+    __syncthreads();
+    return last;
+}
+
+__device__ __forceinline__ unsigned load4(const unsigned char *p, unsigned long long avail) {
+    if (avail >= 4 && ((uintptr_t)p & 3) == 0) return *reinterpret_cast<const unsigned *>(p);
+    unsigned v = 0;
+    for (unsigned b = 0; b < 4 && b < avail; ++b) v |= (unsigned)p[b] << (8 * b);
+    return v;
+}
+
+__device__ __forceinline__ void store4(unsigned char *p, unsigned v, unsigned long long room) {
+    if (room >= 4 && ((uintptr_t)p & 3) == 0) {
+        *reinterpret_cast<unsigned *>(p) = v;
+        return;
+    }
+    for (unsigned b = 0; b < 4 && b < room; ++b) p[b] = (unsigned char)(v >> (8 * b));
+}
+
+__global__ void __launch_bounds__(256)
+chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
+                 unsigned long long timeout_ns, int *err) {
+    __shared__ int ok;
+    __shared__ unsigned long long k;
+    if (threadIdx.x == 0) {
+        k = *(volatile unsigned long long *)c.seq;
+        // slot k % depth is free once the receiver consumed message k - depth
+        ok = k < (unsigned long long)c.depth ||
+             hx::spin_until(c.credit, k + 1 - c.depth, timeout_ns, err, 0);
+    }
+    __syncthreads();
+    char *slot = c.slots + (k % c.depth) * c.stride;
+    unsigned long long *hdr = reinterpret_cast<unsigned long long *>(slot);
+    const unsigned long long tag = (k + 1) & 0xffffffffull;
+    if (bytes <= HX_CHAN_LL_MAX) {  // single CTA: LL words, no fence
+        if (ok) {
+            unsigned long long *words = reinterpret_cast<unsigned long long *>(slot + CHAN_HDR);
+            const unsigned long long n = (bytes + 3) / 4;
+            for (unsigned long long w = threadIdx.x; w < n; w += blockDim.x)
+                st_relaxed_sys(words + w, (tag << 32) | load4(src + 4 * w, bytes - 4 * w));
+            if (threadIdx.x == 0) {
+                st_relaxed_sys(hdr, (tag << 32) | bytes);
+                *c.seq = k + 1;
+            }
+        }
+        return;
+    }
+    if (ok)
+        copy_bytes(slot + CHAN_HDR, (const char *)src, bytes,
+                   blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x,
+                   false);
+    if (chan_last_cta(c.counter) && threadIdx.x == 0 && ok) {
+        hx::st_release_sys(hdr, (tag << 32) | bytes);  // release: orders every CTA's payload
+        *c.seq = k + 1;
+    }
+}
+
+__global__ void __launch_bounds__(256)
+chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
+                 unsigned long long *len_out, unsigned long long timeout_ns, int *err) {
+    __shared__ int ok;
+    __shared__ unsigned long long k, len;
+    if (threadIdx.x == 0) {
+        k = *(volatile unsigned long long *)c.seq;
+        const unsigned long long tag = (k + 1) & 0xffffffffull;
+        const unsigned long long *hdr =
+            reinterpret_cast<const unsigned long long *>(c.slots + (k % c.depth) * c.stride);
+        const unsigned long long t0 = hx::globaltimer();
+        unsigned long long h;
+        unsigned polls = 0;
+        ok = 1;
+        while (((h = ld_relaxed_sys(hdr)) >> 32) != tag) {
+            if ((++polls & 63) == 0 && hx::globaltimer() - t0 > timeout_ns) {
+                atomicExch(err, HX_E_TIMEOUT);
+                ok = 0;
+                break;
+            }
+        }
+        len = h & 0xffffffffull;
+        if (ok && len > HX_CHAN_LL_MAX) (void)hx::ld_acquire_sys(hdr);  // bulk: order the payload
+    }
+    __syncthreads();
+    const char *slot = c.slots + (k % c.depth) * c.stride;
+    const unsigned long long take = len < capacity ? len : capacity;
+    const unsigned long long tag = (k + 1) & 0xffffffffull;
+    if (ok && len <= HX_CHAN_LL_MAX) {
+        const unsigned long long *words = reinterpret_cast<const unsigned long long *>(slot + CHAN_HDR);
+        const unsigned long long n = (take + 3) / 4;
+        for (unsigned long long w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n;
+             w += (size_t)gridDim.x * blockDim.x) {
+            unsigned long long v;
+            unsigned polls = 0;
+            const unsigned long long t0 = hx::globaltimer();
+            while (((v = ld_relaxed_sys(words + w)) >> 32) != tag) {
+                if ((++polls & 255) == 0 && hx::globaltimer() - t0 > timeout_ns) {
+                    atomicExch(err, HX_E_TIMEOUT);
+                    break;
+                }
+            }
+            store4(dst + 4 * w, (unsigned)v, take - 4 * w);
+        }
+    } else if (ok) {
+        copy_bytes((char *)dst, slot + CHAN_HDR, take,
+                   blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x,
+                   true);
+    }
+    if (chan_last_cta(c.counter) && threadIdx.x == 0 && ok) {
+        if (len_out) *len_out = len;  // > capacity: the caller reports truncation
+        // every thread's slot reads fed its stores before the barrier, so
+        // the slot may be handed back without a fence
+        st_relaxed_sys(c.credit, k + 1);
+        *c.seq = k + 1;
+    }
+}
+
 // Low-latency (LL) ping-pong: every 8-byte word carries 4 payload bytes and
 // the 32-bit iteration tag, written with one single-copy-atomic store, so
 // the receiver polls the data itself — no fence, no separate flag.
@@ -513,6 +662,43 @@ int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream, 
     if (done_event) HX_TRY(cudaEventRecord((cudaEvent_t)done_event, st));
     if (order_stream && done_event)
         HX_TRY(cudaStreamWaitEvent((cudaStream_t)order_stream, (cudaEvent_t)done_event, 0));
+    return 0;
+}
+
+static unsigned chan_grid(unsigned long long bytes) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const unsigned long long want = (bytes + 16383) / 16384;  // ~16 KiB per CTA
+    return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, 2ull * sms));
+}
+
+int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int depth,
+                 unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
+                 unsigned long long timeout_ns, int *err, void *stream) {
+    if (!slots || !credit || !seq || !counter || depth < 1 || (bytes && !src)) return HX_E_INVALID;
+    const unsigned long long need =
+        CHAN_HDR + (bytes <= HX_CHAN_LL_MAX ? 8 * ((bytes + 3) / 4) : bytes);
+    if (need > stride || bytes > 0xffffffffull) return HX_E_INVALID;
+    ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
+    const unsigned grid = bytes <= HX_CHAN_LL_MAX ? 1u : chan_grid(bytes);
+    chan_send_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c, (const unsigned char *)src, bytes,
+                                                             timeout_ns, err);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
+int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, int depth,
+                 unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
+                 unsigned long long *len_out, unsigned long long timeout_ns, int *err,
+                 void *stream) {
+    if (!slots || !credit || !seq || !counter || depth < 1 || (capacity && !dst))
+        return HX_E_INVALID;
+    ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
+    chan_recv_kernel<<<chan_grid(std::min<unsigned long long>(capacity, stride)), 256, 0,
+                       (cudaStream_t)stream>>>(c, (unsigned char *)dst, capacity, len_out,
+                                               timeout_ns, err);
+    HX_LAUNCH_CHECK();
     return 0;
 }
 

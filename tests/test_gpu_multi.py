@@ -104,3 +104,54 @@ def test_p2p_engine_at_scale_across_gpus(cuda, exchange, overlap):
     got = eng.assemble()
     eng.close()
     assert np.array_equal(got, want)
+
+
+@needs2
+@pytest.mark.parametrize("depth", [1, 3])
+def test_persistent_channel_stream_ordered_exchange(cuda, depth):
+    """pchannel.PersistentChannel: 40 messages each way with random sizes
+    (0 B to the slot size) through a ring of `depth` slots, both directions
+    interleaved, payloads bit-exact and in order; a receive with less
+    capacity than the message reports TRUNCATED with the full length."""
+    from paper_2102_12416_b200.completion import OK, TRUNCATED
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    rng = np.random.default_rng(depth)
+    slot = 70000
+    ch = PersistentChannel(0, 1, slot_bytes=slot, depth=depth, timeout_s=20)
+    s = [torch.cuda.Stream(device=0), torch.cuda.Stream(device=1)]
+    sizes = [int(x) for x in rng.integers(0, slot + 1, 40)]
+    sizes[3], sizes[7] = slot, 1
+    msgs = [[torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8)).to(f"cuda:{e}")
+             for n in sizes] for e in (0, 1)]
+    sinks = [[torch.zeros(slot, dtype=torch.uint8, device=f"cuda:{1 - e}") for _ in sizes]
+             for e in (0, 1)]
+    tickets = [[], []]
+    for k, n in enumerate(sizes):  # endpoint 0 sends k, endpoint 1 sends k; both receive
+        for e in (0, 1):
+            ch.send(e, msgs[e][k], n, stream=s[e])
+        for e in (0, 1):
+            tickets[e].append(ch.recv(1 - e, sinks[e][k], slot, stream=s[1 - e]))
+    ch.check()
+    for e in (0, 1):
+        for k, n in enumerate(sizes):
+            st, length = ch.completion(1 - e, tickets[e][k], slot)
+            assert st == OK and length == n
+            assert torch.equal(sinks[e][k][:n].cpu(), msgs[e][k].cpu()), (e, k)
+    assert ch.counters == [(40, 40), (40, 40)]
+    small = torch.zeros(10, dtype=torch.uint8, device="cuda:1")
+    ch.send(0, msgs[0][3], slot, stream=s[0])
+    t = ch.recv(1, small, 10, stream=s[1])
+    assert ch.completion(1, t, 10) == (TRUNCATED, slot)
+    assert torch.equal(small.cpu(), msgs[0][3][:10].cpu())
+
+
+@needs2
+@pytest.mark.parametrize("size", [8, 4096, 1 << 20])
+def test_persistent_channel_osu_graphs(cuda, size):
+    from paper_2102_12416_b200.osu import channel_bandwidth, channel_latency
+
+    lat = channel_latency(size, iters=200, warmup=20)
+    assert lat["verified"] and 0 < lat["value_ns"] < 1e6
+    bw = channel_bandwidth(size, window=16, iters=3)
+    assert bw["verified"] and bw["value_gbps"] > 0

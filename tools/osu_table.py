@@ -29,6 +29,8 @@ def main():
         ("msg dev lat", lambda s: lat(pick(s, benchmark="latency", api="charm-messaging", mode="device"))),
         ("mpi dev lat", lambda s: lat(pick(s, benchmark="latency", api="mpi", mode="device"))),
         ("chan host-staged lat", lambda s: lat(pick(s, benchmark="latency", api="charm-channel", mode="host"))),
+        ("persistent chan lat (µs)", lambda s: lat(pick(s, benchmark="channel-latency"))),
+        ("persistent chan bw (GB/s)", lambda s: bw(pick(s, benchmark="channel-bandwidth"))),
         ("chan dev bw (GB/s)", lambda s: bw(pick(s, benchmark="bandwidth", api="charm-channel", mode="device"))),
         ("msg dev bw", lambda s: bw(pick(s, benchmark="bandwidth", api="charm-messaging", mode="device"))),
         ("device lat (µs)", lambda s: lat(pick(s, benchmark="device-latency"))),

@@ -3,6 +3,8 @@
 API level (the reference's measure_latency / measure_bandwidth procedures,
 cl/bench.py:364-452, through the drop-in runtime): charm-channel,
 charm-messaging and mpi, device mode, plus host-staging for contrast.
+Persistent channel (pchannel: pre-registered slots, device-side counters,
+per-GPU CUDA graphs): ping-pong latency and window bandwidth.
 Device level: kernel-issued NVLink ping-pong (globaltimer) and windowed
 peer-copy bandwidth (copy engine and SM stores, CUDA events).
 
@@ -26,8 +28,9 @@ def main():
 
     import torch
 
-    from paper_2102_12416_b200.osu import (device_bandwidth, device_latency, measure_bandwidth,
-                                           measure_latency, parse_sizes)
+    from paper_2102_12416_b200.osu import (channel_bandwidth, channel_latency, device_bandwidth,
+                                           device_latency, measure_bandwidth, measure_latency,
+                                           parse_sizes)
 
     ngpu = torch.cuda.device_count()
     sizes = parse_sizes("8:4194304:x2")
@@ -50,6 +53,8 @@ def main():
             r = measure_bandwidth(api, "device", size, window=64, iters=5, warmup=2)
             emit({**r, "level": "api", "gpus": min(ngpu, 2)})
         if ngpu >= 2:
+            emit(channel_latency(size, iters=1000 if size <= 65536 else 200, warmup=20))
+            emit(channel_bandwidth(size, window=64, iters=5))
             emit({**device_latency(size, iters=2000 if size <= 65536 else 200, warmup=50),
                   "level": "device"})
             for engine in ("ce", "sm", "sm-pull", "sm-window", "sm-pull-window"):
