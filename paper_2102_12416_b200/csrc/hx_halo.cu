@@ -295,6 +295,16 @@ __device__ __forceinline__ bool chan_last_cta(unsigned int *counter) {
     return last;
 }
 
+// Programmatic dependent launch: channel kernels are launched with
+// programmatic stream serialisation, so the next operation on the stream is
+// scheduled while this one runs; each still waits for its predecessor's
+// completion (and memory) before it touches the channel state. The device
+// counters keep the exact stream order; only the launch latency overlaps.
+__device__ __forceinline__ void chan_dependent_prologue() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned load4(const unsigned char *p, unsigned long long avail) {
     if (avail >= 4 && ((uintptr_t)p & 3) == 0) return *reinterpret_cast<const unsigned *>(p);
     unsigned v = 0;
@@ -315,6 +325,7 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
                  unsigned long long timeout_ns, int *err) {
     __shared__ int ok;
     __shared__ unsigned long long k;
+    chan_dependent_prologue();
     if (threadIdx.x == 0) {
         k = *(volatile unsigned long long *)c.seq;
         // slot k % depth is free once the receiver consumed message k - depth
@@ -353,6 +364,7 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                  unsigned long long *len_out, unsigned long long timeout_ns, int *err) {
     __shared__ int ok;
     __shared__ unsigned long long k, len;
+    chan_dependent_prologue();
     if (threadIdx.x == 0) {
         k = *(volatile unsigned long long *)c.seq;
         const unsigned long long tag = (k + 1) & 0xffffffffull;
@@ -673,6 +685,19 @@ static unsigned chan_grid(unsigned long long bytes) {
     return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, 2ull * sms));
 }
 
+static cudaLaunchConfig_t chan_launch_config(unsigned grid, void *stream, cudaLaunchAttribute *attr) {
+    attr->id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr->val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = (cudaStream_t)stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+
 int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int depth,
                  unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
                  unsigned long long timeout_ns, int *err, void *stream) {
@@ -682,9 +707,10 @@ int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int 
     if (need > stride || bytes > 0xffffffffull) return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
     const unsigned grid = bytes <= HX_CHAN_LL_MAX ? 1u : chan_grid(bytes);
-    chan_send_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c, (const unsigned char *)src, bytes,
-                                                             timeout_ns, err);
-    HX_LAUNCH_CHECK();
+    cudaLaunchAttribute attr;
+    const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
+    HX_TRY(cudaLaunchKernelEx(&cfg, chan_send_kernel, c, (const unsigned char *)src,
+                              (unsigned long long)bytes, timeout_ns, err));
     return 0;
 }
 
@@ -695,10 +721,11 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
     if (!slots || !credit || !seq || !counter || depth < 1 || (capacity && !dst))
         return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
-    chan_recv_kernel<<<chan_grid(std::min<unsigned long long>(capacity, stride)), 256, 0,
-                       (cudaStream_t)stream>>>(c, (unsigned char *)dst, capacity, len_out,
-                                               timeout_ns, err);
-    HX_LAUNCH_CHECK();
+    cudaLaunchAttribute attr;
+    const cudaLaunchConfig_t cfg =
+        chan_launch_config(chan_grid(std::min<unsigned long long>(capacity, stride)), stream, &attr);
+    HX_TRY(cudaLaunchKernelEx(&cfg, chan_recv_kernel, c, (unsigned char *)dst,
+                              (unsigned long long)capacity, len_out, timeout_ns, err));
     return 0;
 }
 
