@@ -577,25 +577,30 @@ int num_sms() {
     return g_num_sms;
 }
 
+// Function attributes live in each device's context: set them once per
+// device (a process driving several GPUs launches on each; `done` holds a
+// bit per ordinal) and ask for the full shared-memory carveout so that
+// 3 CTAs of ~74 KB fit per SM.
+template <typename Kernel>
+int ensure_smem(Kernel kernel, size_t bytes, unsigned long long &done) {
+    int dev = 0;
+    HX_TRY(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (!(done & bit)) {
+        HX_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+        HX_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    (int)cudaSharedmemCarveoutMaxShared));
+        done |= bit;
+    }
+    return 0;
+}
+
 template <bool RES, int BOX_Z>
 int launch_tma_t(const CUtensorMap &map, double *nxt, int by, int bz, int i0, int i1, int j0,
                  int j1, int k0, int k1, int ntj, int ntk, int chunk, int nchunks, int grows, long items,
                  unsigned long long *res, cudaStream_t st) {
-    // Function attributes live in each device's context: set them once per
-    // device (a process driving several GPUs launches this on each), and ask
-    // for the full shared-memory carveout so 3 CTAs (3 x 74 KB) fit per SM.
-    static unsigned long long attr_set = 0;  // bit per device ordinal
-    int dev = 0;
-    HX_TRY(cudaGetDevice(&dev));
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(attr_set & bit)) {
-        HX_TRY(cudaFuncSetAttribute(stencil_tma_kernel<RES, BOX_Z>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM_BYTES));
-        HX_TRY(cudaFuncSetAttribute(stencil_tma_kernel<RES, BOX_Z>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared));
-        attr_set |= bit;
-    }
+    static unsigned long long attr_set = 0;
+    if (int rc = ensure_smem(stencil_tma_kernel<RES, BOX_Z>, SMEM_BYTES, attr_set)) return rc;
     stencil_tma_kernel<RES, BOX_Z><<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
         map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk, chunk, nchunks, grows, res);
     HX_LAUNCH_CHECK();
@@ -696,18 +701,8 @@ int pair_maps_for(const double *cur, int bx, int by, int bz, PairMaps *out) {
 template <bool RES>
 int launch_pair_t(const PairMaps &pm, double *nxt, int by, int bz, int i0, int i1, int j0, int j1,
                   int k0, int k1, const Schedule &sc, unsigned long long *res, cudaStream_t st) {
-    static unsigned long long attr_set = 0;  // per device, as for the TMA kernel
-    int dev = 0;
-    HX_TRY(cudaGetDevice(&dev));
-    const unsigned long long bit = 1ull << (dev & 63);
-    if (!(attr_set & bit)) {
-        HX_TRY(cudaFuncSetAttribute(stencil_pair_kernel<RES>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PSMEM_BYTES));
-        HX_TRY(cudaFuncSetAttribute(stencil_pair_kernel<RES>,
-                                    cudaFuncAttributePreferredSharedMemoryCarveout,
-                                    (int)cudaSharedmemCarveoutMaxShared));
-        attr_set |= bit;
-    }
+    static unsigned long long attr_set = 0;
+    if (int rc = ensure_smem(stencil_pair_kernel<RES>, PSMEM_BYTES, attr_set)) return rc;
     stencil_pair_kernel<RES><<<(unsigned)sc.items, THREADS, PSMEM_BYTES, st>>>(
         pm, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk, sc.chunk, sc.nchunks, sc.grows,
         res);
