@@ -526,9 +526,13 @@ std::map<std::tuple<const void *, int, int, int, int, int>, CUtensorMap> g_maps;
 
 int l2_promotion() {
     if (g_l2promo < 0) {
-        const char *e = getenv("HX_TMA_L2PROMO");  // 0 none, 1 64B, 2 128B, 3 256B
-        g_l2promo = e ? atoi(e) : 1;
-        if (g_l2promo < 0 || g_l2promo > 3) g_l2promo = 1;
+        // 0 none, 1 64B, 2 128B, 3 256B. Measured (tools/sweep_tma_knobs.sh):
+        // 256-byte promotion is fastest for every sweep shape — 1536^3
+        // 8.883 ms vs 8.927 (64B), 1535^3 8.831 vs 8.877, 768x1536x3072
+        // 8.816 vs 8.862.
+        const char *e = getenv("HX_TMA_L2PROMO");
+        g_l2promo = e ? atoi(e) : 3;
+        if (g_l2promo < 0 || g_l2promo > 3) g_l2promo = 3;
     }
     return g_l2promo;
 }
