@@ -174,13 +174,16 @@ int hx_wait_unpack(double *field, int bx, int by, int bz, int dir_mask,
  * the last CTA's stores are visible system-wide it release-stores
  * signal_value into every non-NULL signal_flag[d] (skipped if *err != 0).
  * counter: one zero-initialised uint32 that the kernel returns to zero.
- * res: optional max|nxt-cur| accumulator, as for hx_stencil. */
+ * res: optional max|nxt-cur| accumulator, as for hx_stencil.
+ * step (nullable): a device uint64 iteration counter; when given, both
+ * values are offsets from *step and the last CTA advances *step by one, so
+ * a step sequence can be captured once in a CUDA graph and replayed. */
 int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbox,
                  const int *boxes, double *const remote[6],
                  unsigned long long *const wait_flag[6], unsigned long long wait_value,
                  unsigned long long *const signal_flag[6], unsigned long long signal_value,
                  unsigned int *counter, unsigned long long timeout_ns, int *err,
-                 unsigned long long *res, void *stream);
+                 unsigned long long *res, unsigned long long *step, void *stream);
 
 /* --------------------------------------------------- persistent channel --
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper

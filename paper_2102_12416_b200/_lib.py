@@ -106,7 +106,7 @@ _SIGS = {
     "hx_wait_unpack": ([_V, _I, _I, _I, _I, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64, _U64,
                         _V, _V], _I),
     "hx_shell_put": ([_V, _V, _I, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64,
-                      ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V], _I),
+                      ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V, _V], _I),
     "hx_chan_send": ([_V, _SZ, _V, _SZ, _I, _V, _V, _V, _U64, _V, _V], _I),
     "hx_chan_recv": ([_V, _SZ, _V, _SZ, _I, _V, _V, _V, _V, _U64, _V, _V], _I),
     "hx_signal": ([_V, _U64, _V], _I),

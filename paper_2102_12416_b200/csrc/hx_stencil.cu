@@ -456,12 +456,14 @@ __global__ void __launch_bounds__(256)
 shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
                  ShellJob J, unsigned long long wait_value, unsigned long long signal_value,
                  unsigned *counter, unsigned long long timeout_ns, int *err,
-                 unsigned long long *res) {
+                 unsigned long long *res, unsigned long long *step) {
     __shared__ int ok;
+    __shared__ unsigned long long base;  // device step counter (graph replays), else 0
     if (threadIdx.x == 0) {
+        base = step ? *(volatile unsigned long long *)step : 0ull;
         ok = 1;
         for (int d = 0; d < 6 && ok; ++d)
-            if (J.wait[d]) ok = hx::spin_until(J.wait[d], wait_value, timeout_ns, err);
+            if (J.wait[d]) ok = hx::spin_until(J.wait[d], base + wait_value, timeout_ns, err);
     }
     __syncthreads();
     const hx::Geom g(by, bz);
@@ -509,7 +511,8 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
             __threadfence_system();
             const bool healthy = !err || *(volatile int *)err == 0;
             for (int d = 0; d < 6 && healthy; ++d)
-                if (J.signal[d]) hx::st_release_sys(J.signal[d], signal_value);
+                if (J.signal[d]) hx::st_release_sys(J.signal[d], base + signal_value);
+            if (step) *step = base + 1;  // every CTA read it before this last one counted
         }
     }
 }
@@ -899,14 +902,15 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
                  const int *boxes, double *const remote[6], unsigned long long *const wait_flag[6],
                  unsigned long long wait_value, unsigned long long *const signal_flag[6],
                  unsigned long long signal_value, unsigned int *counter,
-                 unsigned long long timeout_ns, int *err, unsigned long long *res, void *stream) {
+                 unsigned long long timeout_ns, int *err, unsigned long long *res,
+                 unsigned long long *step, void *stream) {
     if (!cur || !nxt || !counter || bx < 1 || by < 1 || bz < 1 || nbox < 0 || nbox > 6)
         return HX_E_INVALID;
     if (nbox > 0 && !boxes) return HX_E_INVALID;
     ShellJob J;
     memset(&J, 0, sizeof(J));
     const long long sx = (long long)(by + 2) * (bz + 2), sy = bz + 2;
-    const long long step[3] = {sx * bx, sy * by, (long long)bz};
+    const long long span[3] = {sx * bx, sy * by, (long long)bz};  // block extent per axis
     const int ext[3] = {bx, by, bz};
     for (int d = 0; d < 6; ++d) {
         J.remote[d] = remote ? remote[d] : nullptr;
@@ -915,7 +919,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         // our plane 1 (d even) is the neighbour's ghost plane ext+1, our
         // plane ext (d odd) its ghost plane 0
         J.face[d] = (d & 1) ? ext[d >> 1] : 1;
-        J.shift[d] = (d & 1) ? -step[d >> 1] : step[d >> 1];
+        J.shift[d] = (d & 1) ? -span[d >> 1] : span[d >> 1];
     }
     J.start[0] = 0;
     for (int q = 0; q < nbox; ++q) {
@@ -938,7 +942,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>((n + 255) / 256, (long long)mult * num_sms()));
     shell_put_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
-        cur, nxt, by, bz, J, wait_value, signal_value, counter, timeout_ns, err, res);
+        cur, nxt, by, bz, J, wait_value, signal_value, counter, timeout_ns, err, res, step);
     HX_LAUNCH_CHECK();
     return 0;
 }

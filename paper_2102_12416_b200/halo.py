@@ -90,6 +90,7 @@ class HaloBlock:
             shape = (self.bx + 2, self.by + 2, self.bz + 2)
             self.fields = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
             self.arena = torch.zeros(self.arena_bytes, dtype=torch.uint8, device=dev)
+            self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)  # graph replays
         # filled by HaloJacobi.connect(): (neighbour arena base, its side)
         self.put_dst = [None] * NDIRS
         self.put_flag = [None] * NDIRS
@@ -112,6 +113,10 @@ class HaloBlock:
 
     def flag_ptr(self, d: int, base: int | None = None) -> int:
         return (self.base if base is None else base) + 8 * d
+
+    @property
+    def step_ptr(self) -> int:
+        return self.step_dev.data_ptr()
 
     @property
     def counters_ptr(self) -> int:
@@ -208,6 +213,7 @@ class HaloJacobi:
         self.it = 0
         self._ipc_bases = []
         self._res = {}
+        self._graphs = {}  # buffer parity -> {device: CUDAGraph} (run_graph)
         self.reset()
         if exchange in ("p2p", "fused"):
             self.connect()
@@ -495,18 +501,22 @@ class HaloJacobi:
                 _lib.call("hx_set_device", b.device)
                 self._wait(b, 0)
 
-    def _step_fused(self, residual, timing) -> None:
+    def _step_fused(self, residual, timing, devices=None, dev_step=False) -> None:
         """exchange="fused": per block, the comm stream runs ONE kernel that
         waits for the neighbours' previous boundary, relaxes the boundary
         shell and stores the neighbour-facing planes straight into the
         neighbours' nxt ghost planes over NVLink, then releases their flags
         (hx_shell_put); the main stream sweeps the interior concurrently.
         The step's work is complete on the main stream (it waits for the
-        shell), so the next interior sees this step's boundary."""
+        shell), so the next interior sees this step's boundary.
+
+        devices: only the blocks on these GPUs (graph capture, one graph per
+        GPU); dev_step: flag values come from each block's device step
+        counter instead of the host's iteration number (graph replays)."""
         it = self.it
         if it == 0:
             self._prime()
-        blocks = list(self.blocks.values())
+        blocks = [b for b in self.blocks.values() if devices is None or b.device in devices]
         mark = _Marks(timing)
         shell_done = {}
         for b in blocks:
@@ -523,11 +533,13 @@ class HaloJacobi:
             remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
             wait = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
             signal = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+            base = 0 if dev_step else it
             mark.begin("exchange", b, c)
             _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
-                      len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array(wait), it + 1,
-                      _lib.ptr_array(signal), it + 2, b.counters_ptr + 4, self.timeout_ns,
-                      b.err_ptr, self._res_ptr(b, it, residual), c.cuda_stream)
+                      len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array(wait), base + 1,
+                      _lib.ptr_array(signal), base + 2, b.counters_ptr + 4, self.timeout_ns,
+                      b.err_ptr, self._res_ptr(b, it, residual),
+                      b.step_ptr if dev_step else None, c.cuda_stream)
             mark.end("exchange", b, c)
             ev = torch.cuda.Event()
             ev.record(c)
@@ -552,6 +564,49 @@ class HaloJacobi:
             mark.end("sweep", b, s)
             b.cur ^= 1
         self.it += 1
+
+    def run_graph(self, iters: int) -> None:
+        """``iters`` fused iterations replayed from CUDA graphs: two steps
+        (one buffer-parity period) of every local block are captured once
+        per GPU, and each graph is replayed with the flag values taken from
+        the blocks' device step counters, so the host enqueues one launch
+        per GPU per two iterations. Same kernels and bits as run(); no
+        residual or timing. GPUs synchronise only through the channel
+        flags, whose waits always point at an earlier step."""
+        if self.exchange != "fused":
+            raise ValueError("run_graph needs exchange='fused'")
+        if iters <= 0:
+            return
+        if self.it == 0:  # the priming exchange and step 0 stay outside the graph
+            self.step()
+            iters -= 1
+        parity = next(iter(self.blocks.values())).cur
+        graphs = self._graphs.get(parity)
+        if graphs is None:
+            graphs = self._graphs[parity] = self._capture_pair()
+        for b in self.blocks.values():
+            with torch.cuda.stream(self.stream_of(b)):
+                b.step_dev.fill_(self.it)
+        for _ in range(iters // 2):
+            for d, g in graphs.items():
+                with torch.cuda.device(d), torch.cuda.stream(self.streams[d]):
+                    g.replay()
+        self.it += 2 * (iters // 2)
+        if iters % 2:
+            self.step()
+
+    def _capture_pair(self) -> dict:
+        self.synchronize()
+        graphs = {}
+        for d, s in self.streams.items():
+            g = torch.cuda.CUDAGraph()
+            it0 = self.it
+            with torch.cuda.device(d), torch.cuda.graph(g, stream=s):
+                for _ in range(2):
+                    self._step_fused(False, None, devices={d}, dev_step=True)
+            self.it = it0  # capture only recorded the steps (each block flipped twice)
+            graphs[d] = g
+        return graphs
 
     def run(self, iters: int, residual: bool = False) -> None:
         for _ in range(iters):

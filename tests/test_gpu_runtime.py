@@ -481,3 +481,22 @@ def test_osu_cli(pkg, tmp_path):
     assert main(["--benchmark", "latency", "--api", "charm-channel", "--sizes", "8,4096",
                  "--iters", "3", "--csv", str(out)]) == 0
     assert out.read_text().splitlines()[0] == "benchmark,api,mode,size_bytes,metric,value,unit,time_mode"
+
+
+@pytest.mark.parametrize("pes,dims,iters", [(1, (32, 32, 32), 9), (2, (64, 64, 64), 20),
+                                            (8, (64, 64, 64), 21), (6, (24, 18, 30), 11)])
+def test_fused_graph_replay_matches(pkg, pes, dims, iters):
+    """HaloJacobi.run_graph (per-GPU CUDA graphs of two fused steps, flag
+    values from device step counters) gives the eager path's bits, for odd
+    and even iteration counts and after eager steps."""
+    from oracle import jacobi_np
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, policy="b200", exchange="fused")
+    eng.run(3)
+    eng.run_graph(iters - 5)
+    eng.run(2)
+    eng.check_errors()
+    want, _ = jacobi_np.sequential(dims, iters)
+    assert eng.assemble().tobytes() == want.tobytes()
+    eng.close()

@@ -57,7 +57,7 @@ def main():
                 _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
                           len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array([None] * 6), 0,
                           _lib.ptr_array([None] * 6), 0, b.counters_ptr + 4, eng.timeout_ns,
-                          b.err_ptr, None, c.cuda_stream)
+                          b.err_ptr, None, None, c.cuda_stream)
                 e1.record(c)
                 c.synchronize()
                 iso.append(e0.elapsed_time(e1))
