@@ -42,12 +42,13 @@ def test_p2p_engine_across_gpus(cuda, pes, exchange, overlap):
 
 
 @needs2
-@pytest.mark.parametrize("mode", ["0", "1", "fused"])
+@pytest.mark.parametrize("mode", ["0", "1", "fused", "graph"])
 def test_ipc_engine_under_torchrun(cuda, tmp_path, mode):
     out = tmp_path / "verdict.json"
     n = 4 if ngpu() >= 4 else 2
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(29533 + ["0", "1", "fused"].index(mode)),
+           "--master-addr", "127.0.0.1",
+           "--master-port", str(29533 + ["0", "1", "fused", "graph"].index(mode)),
            os.path.join(ROOT, "tests", "mp_halo_worker.py"), "48", "32", "40", "15", str(out),
            mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
@@ -155,3 +156,20 @@ def test_persistent_channel_osu_graphs(cuda, size):
     assert lat["verified"] and 0 < lat["value_ns"] < 1e6
     bw = channel_bandwidth(size, window=16, iters=3)
     assert bw["verified"] and bw["value_gbps"] > 0
+
+
+@needs2
+@pytest.mark.parametrize("pes", [2, 8])
+def test_fused_graph_replay_across_gpus(cuda, pes):
+    """run_graph with blocks on two GPUs: each GPU replays its own graph and
+    the GPUs meet only through the channel flags."""
+    from oracle import jacobi_np
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    dims = (48, 32, 40)
+    eng = HaloJacobi(dims, pes, device_of=lambda r: r % 2, timeout_s=20, exchange="fused")
+    eng.run_graph(17)
+    eng.check_errors()
+    want, _ = jacobi_np.sequential(dims, 17)
+    assert eng.assemble().tobytes() == want.tobytes()
+    eng.close()
