@@ -193,8 +193,12 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
  * 32 bits and the length in the low 32, i.e. the arrival flag and the length
  * in one word — then the payload. Payloads up to HX_CHAN_LL_MAX bytes go as
  * LL words (8-byte stores of 4 data bytes + the tag: no fences, the receiver
- * polls the data), larger ones as a bulk copy published by a release store
- * of the header. The message index is device state (*seq, one per endpoint,
+ * polls the data), payloads that fit a slot as a bulk copy into it
+ * published by a release store of the header (the sender may run `depth`
+ * messages ahead); larger ones are pulled: the header publishes the source
+ * address and the receive copies straight out of the sender's buffer over
+ * NVLink (one copy, any size below 2^31 bytes), the send completing when
+ * the slot comes back. The message index is device state (*seq, one per endpoint,
  * advanced by each launch), so send/recv sequences can be captured in CUDA
  * graphs.
  *   send k: wait until *credit >= k+1-depth (slot k % depth free), write
@@ -202,7 +206,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
  *   recv k: wait for the header tag, copy min(len, capacity) bytes into dst,
  *           write len to *len_out (nullable; len > capacity = truncated) and
  *           store *credit = k+1 (a peer-mapped pointer).
- * stride must cover 16 + the payload (16 + 8 * ceil(bytes / 4) for LL).
+ * stride must hold 16 + 8 * ceil(min(bytes, HX_CHAN_LL_MAX) / 4) (LL messages).
  * counter: one zero-initialised uint32 per endpoint and direction. Waits
  * are bounded by timeout_ns (then *err = HX_E_TIMEOUT). */
 #define HX_CHAN_LL_MAX 8192u

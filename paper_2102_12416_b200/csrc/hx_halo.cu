@@ -277,7 +277,8 @@ struct ChanDir {
     int depth;
 };
 
-constexpr unsigned long long CHAN_HDR = 16;
+constexpr unsigned long long CHAN_HDR = 16;      // [header][source pointer (pull)]
+constexpr unsigned long long CHAN_PULL = 1ull << 31;  // header length flag: pull from the source
 
 // True in the CTA that finishes last (after every CTA's copy). A single CTA
 // needs no counter: the barrier orders its threads' stores before thread
@@ -349,6 +350,17 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
         }
         return;
     }
+    if (bytes > HX_CHAN_LL_MAX && CHAN_HDR + bytes > c.stride) {
+        // does not fit a slot: single CTA publishes the source, waits for the pull
+        if (ok && threadIdx.x == 0) {
+            st_relaxed_sys(hdr + 1, (unsigned long long)(uintptr_t)src);
+            hx::st_release_sys(hdr, (tag << 32) | CHAN_PULL | bytes);  // orders the pointer
+            // the receiver copies straight out of src over NVLink; src is
+            // reusable (the send complete) once it hands the slot back
+            if (hx::spin_until(c.credit, k + 1, timeout_ns, err, 0)) *c.seq = k + 1;
+        }
+        return;
+    }
     if (ok)
         copy_bytes(slot + CHAN_HDR, (const char *)src, bytes,
                    blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x,
@@ -363,7 +375,9 @@ __global__ void __launch_bounds__(256)
 chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                  unsigned long long *len_out, unsigned long long timeout_ns, int *err) {
     __shared__ int ok;
+    __shared__ bool pull;
     __shared__ unsigned long long k, len;
+    __shared__ const char *from;
     chan_dependent_prologue();
     if (threadIdx.x == 0) {
         k = *(volatile unsigned long long *)c.seq;
@@ -381,14 +395,21 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                 break;
             }
         }
-        len = h & 0xffffffffull;
-        if (ok && len > HX_CHAN_LL_MAX) (void)hx::ld_acquire_sys(hdr);  // bulk: order the payload
+        pull = (h & CHAN_PULL) != 0;
+        len = h & (CHAN_PULL - 1);
+        if (ok && len > HX_CHAN_LL_MAX) {
+            (void)hx::ld_acquire_sys(hdr);  // bulk / pull: order the payload or the pointer
+            if (pull) from = reinterpret_cast<const char *>(ld_relaxed_sys(hdr + 1));
+        }
     }
     __syncthreads();
     const char *slot = c.slots + (k % c.depth) * c.stride;
     const unsigned long long take = len < capacity ? len : capacity;
     const unsigned long long tag = (k + 1) & 0xffffffffull;
-    if (ok && len <= HX_CHAN_LL_MAX) {
+    if (ok && pull) {  // straight out of the sender's buffer (peer loads, L2 only)
+        copy_bytes((char *)dst, from, take, blockIdx.x * (size_t)blockDim.x + threadIdx.x,
+                   (size_t)gridDim.x * blockDim.x, true);
+    } else if (ok && len <= HX_CHAN_LL_MAX) {
         const unsigned long long *words = reinterpret_cast<const unsigned long long *>(slot + CHAN_HDR);
         const unsigned long long n = (take + 3) / 4;
         for (unsigned long long w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n;
@@ -702,11 +723,12 @@ int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int 
                  unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
                  unsigned long long timeout_ns, int *err, void *stream) {
     if (!slots || !credit || !seq || !counter || depth < 1 || (bytes && !src)) return HX_E_INVALID;
+    const bool pull = bytes > HX_CHAN_LL_MAX && CHAN_HDR + bytes > stride;  // see chan_send_kernel
     const unsigned long long need =
-        CHAN_HDR + (bytes <= HX_CHAN_LL_MAX ? 8 * ((bytes + 3) / 4) : bytes);
-    if (need > stride || bytes > 0xffffffffull) return HX_E_INVALID;
+        CHAN_HDR + (bytes <= HX_CHAN_LL_MAX ? 8 * ((bytes + 3) / 4) : pull ? 0 : bytes);
+    if (need > stride || bytes >= CHAN_PULL) return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
-    const unsigned grid = bytes <= HX_CHAN_LL_MAX ? 1u : chan_grid(bytes);
+    const unsigned grid = (bytes <= HX_CHAN_LL_MAX || pull) ? 1u : chan_grid(bytes);
     cudaLaunchAttribute attr;
     const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_send_kernel, c, (const unsigned char *)src,
@@ -722,8 +744,8 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
         return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
     cudaLaunchAttribute attr;
-    const cudaLaunchConfig_t cfg =
-        chan_launch_config(chan_grid(std::min<unsigned long long>(capacity, stride)), stream, &attr);
+    // sized by the sink: a pulled message may be far larger than a slot
+    const cudaLaunchConfig_t cfg = chan_launch_config(chan_grid(capacity), stream, &attr);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_recv_kernel, c, (unsigned char *)dst,
                               (unsigned long long)capacity, len_out, timeout_ns, err));
     return 0;

@@ -11,9 +11,13 @@ All of it is allocated and mapped once (NVLink P2P between the two GPUs).
 ``send`` is one kernel: wait for a free slot, write the payload into the
 peer's slot over NVLink and publish its header (tag k + 1 and length in one
 word; up to 8 KiB as LL words that carry the tag themselves, so no fence is
-needed; larger payloads are bulk-copied and the header release-stored).
-``recv`` is one kernel: wait for the header tag, copy the slot into the
-sink, hand the slot back (credit = k + 1). The counters (k)
+needed; payloads that fit a slot bulk-copied with the header
+release-stored, so the sender may run ``depth`` messages ahead; larger
+payloads are not copied by the sender at all: the header publishes the
+source address, the receiver copies straight out of it, and the send
+completes when the slot comes back). ``recv`` is one kernel: wait for the
+header tag, copy into the sink, hand the slot back (credit = k + 1). The
+counters (k)
 live on the device, so every operation is stream-ordered like an NCCL call,
 and a sequence of them can be captured in a CUDA graph and replayed with no
 host involvement (``osu.channel_latency`` / ``channel_bandwidth`` do exactly
@@ -36,8 +40,9 @@ LL_MAX = 8192  # include/hx.h HX_CHAN_LL_MAX: payloads up to this go as LL words
 
 class PersistentChannel:
     """Bidirectional channel between endpoint 0 (``gpu_a``) and endpoint 1
-    (``gpu_b``). Messages up to ``slot_bytes``; ``depth`` slots in flight
-    per direction."""
+    (``gpu_b``). Messages up to ``slot_bytes`` are staged in one of
+    ``depth`` slots per direction; larger ones are pulled by the receiver
+    straight from the sender's buffer."""
 
     def __init__(self, gpu_a: int, gpu_b: int, slot_bytes: int = 1 << 20, depth: int = 4,
                  timeout_s: float = 10.0, tickets: int = 4096):
@@ -84,8 +89,6 @@ class PersistentChannel:
         d = self._dir[end]
         gpu = self.gpus[end]
         n = src.numel() * src.element_size() if nbytes is None else nbytes
-        if n > self.slot_bytes:
-            raise ValueError(f"message of {n} bytes exceeds the {self.slot_bytes}-byte slots")
         if src.device != torch.device("cuda", gpu):
             raise ValueError(f"endpoint {end} sends from cuda:{gpu}")
         _lib.call("hx_set_device", gpu)

@@ -173,3 +173,32 @@ def test_fused_graph_replay_across_gpus(cuda, pes):
     want, _ = jacobi_np.sequential(dims, 17)
     assert eng.assemble().tobytes() == want.tobytes()
     eng.close()
+
+
+@needs2
+def test_persistent_channel_pull_mode(cuda):
+    """Messages larger than a slot are pulled by the receiver straight from
+    the sender's buffer (any size): mixed with slot and LL messages on one
+    channel, in order, bit-exact, with truncation."""
+    from paper_2102_12416_b200.completion import OK, TRUNCATED
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    rng = np.random.default_rng(11)
+    ch = PersistentChannel(0, 1, slot_bytes=70000, depth=2, timeout_s=20)
+    s0, s1 = torch.cuda.Stream(device=0), torch.cuda.Stream(device=1)
+    sizes = [70001, 8, 3 << 18, 65000, 5 << 20, 1, 8193, 70000]
+    msgs = [torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8)).to("cuda:0") for n in sizes]
+    sinks = [torch.zeros(max(sizes), dtype=torch.uint8, device="cuda:1") for _ in sizes]
+    tickets = []
+    for m, sink in zip(msgs, sinks):
+        ch.send(0, m, stream=s0)
+        tickets.append(ch.recv(1, sink, stream=s1))
+    ch.check()
+    for n, m, sink, t in zip(sizes, msgs, sinks, tickets):
+        assert ch.completion(1, t, sink.numel()) == (OK, n)
+        assert torch.equal(sink[:n].cpu(), m.cpu())
+    small = torch.zeros(100, dtype=torch.uint8, device="cuda:1")
+    ch.send(0, msgs[4], stream=s0)
+    t = ch.recv(1, small, stream=s1)
+    assert ch.completion(1, t, 100) == (TRUNCATED, 5 << 20)
+    assert torch.equal(small.cpu(), msgs[4][:100].cpu())
