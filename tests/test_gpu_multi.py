@@ -202,3 +202,16 @@ def test_persistent_channel_pull_mode(cuda):
     t = ch.recv(1, small, stream=s1)
     assert ch.completion(1, t, 100) == (TRUNCATED, 5 << 20)
     assert torch.equal(small.cpu(), msgs[4][:100].cpu())
+
+
+@needs2
+def test_osu_cli_channel_benchmarks(cuda, tmp_path):
+    from paper_2102_12416_b200.osu import main
+
+    out = tmp_path / "ch.csv"
+    assert main(["--benchmark", "channel-latency", "--sizes", "8,70000", "--iters", "50",
+                 "--csv", str(out)]) == 0
+    rows = out.read_text().strip().splitlines()
+    assert len(rows) == 3 and rows[1].startswith("channel-latency")
+    assert main(["--benchmark", "channel-bandwidth", "--sizes", "65536", "--window", "8",
+                 "--iters", "2"]) == 0
