@@ -340,8 +340,9 @@ def main() -> int:
                          "kernel_ms": sten_ms,
                          "alg_bytes_per_launch": ALG_BYTES_PER_CELL * sweep_cells},
             "halo": ({"bytes_out_per_rank": face_bytes, "exchange_ms": xch_ms,
-                      "exchange_gbs": face_bytes / (xch_ms * 1e-3) / 1e9,
-                      "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS,
+                      "exchange_gbs": face_bytes / (xch_ms * 1e-3) / 1e9 if xch_ms else None,
+                      "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS if xch_ms
+                      else None,
                       "overlap": eng.overlap, "exposed_ms": exposed_ms,
                       "interior_ms": mean_ms("interior"), "shell_ms": mean_ms("shell"),
                       "non_overlapped_frac": exposed_ms / (t_ms / args.steps),
