@@ -308,6 +308,11 @@ def main() -> int:
     # ---- the exchange alone (not sharing HBM with an interior sweep): a few
     # untimed-for-value steps with the overlap split off, for the NVLink fraction
     iso_ms = None
+    if world > 1 and eng.exchange == "fused":
+        barrier()
+        one = eng.time_shell_alone()
+        barrier()
+        iso_ms = max_over_ranks(one) if one is not None else None
     if world > 1 and eng.exchange == "p2p":
         saved, eng.overlap = eng.overlap, False
         iso: dict = {}

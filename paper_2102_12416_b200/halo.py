@@ -172,8 +172,9 @@ class HaloJacobi:
     """Jacobi3D over persistent NVLink channels.
 
     dims: global grid; pes: total blocks; local_ranks: blocks hosted by this
-    process; device_of(rank) -> CUDA ordinal; group: torch.distributed
-    process group (None when every block is local). policy "reference"
+    process; device_of(rank) -> CUDA ordinal; dist: the initialised
+    torch.distributed module (None when every block is local; used once to
+    exchange IPC handles, and by the NCCL comparison path). policy "reference"
     uses cl/jacobi3d.py's decompose (bit-for-bit the reference's block
     layout); "b200" prefers not to split z on ties.
 
@@ -564,6 +565,34 @@ class HaloJacobi:
             mark.end("sweep", b, s)
             b.cur ^= 1
         self.it += 1
+
+    def time_shell_alone(self, reps: int = 5) -> float | None:
+        """Median ms of one block's hx_shell_put with nothing else running
+        and no flag waits or releases: the fused exchange's own speed (its
+        NVLink stores included). It rewrites exactly the boundary values the
+        next step writes, so the run's state is unchanged."""
+        b = next((b for b in self.blocks.values() if b.nbr_dirs), None)
+        if b is None or self.exchange != "fused":
+            return None
+        _lib.call("hx_set_device", b.device)
+        c = self.comm[b.device]
+        self.synchronize()
+        _, shells = self.boxes(b)
+        flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
+        nxt = b.cur ^ 1
+        remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(c)
+            _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
+                      len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array([None] * 6), 0,
+                      _lib.ptr_array([None] * 6), 0, b.counters_ptr + 4, self.timeout_ns,
+                      b.err_ptr, None, None, c.cuda_stream)
+            e1.record(c)
+            c.synchronize()
+            times.append(e0.elapsed_time(e1))
+        return sorted(times)[len(times) // 2]
 
     def run_graph(self, iters: int) -> None:
         """``iters`` fused iterations replayed from CUDA graphs: two steps
