@@ -444,7 +444,7 @@ __global__ void init_block_kernel(double *f, int bx, int by, int bz, int hot_wal
 struct ShellJob {
     int nbox;
     int box[6][6];          // i0,i1,j0,j1,k0,k1 (1-based, half-open)
-    long long start[7];     // prefix cell counts
+    int rows[7];            // prefix row counts; a row runs along k (along j for a z column)
     double *remote[6];      // neighbour's nxt base (same padded shape), or null
     long long shift[6];     // our padded offset + shift[d] = its ghost cell
     int face[6];            // coordinate of our plane facing d (i/j/k by d/2)
@@ -469,37 +469,52 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
     const hx::Geom g(by, bz);
     const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
     double worst = 0.0;
-    const long long n = J.start[J.nbox];
-    for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; ok && q < n;
-         q += (long long)gridDim.x * blockDim.x) {
+    // One row per CTA iteration: the (box, i, j) decode happens once per row
+    // and the threads stream along it (k-contiguous rows coalesce).
+    for (int row = blockIdx.x; ok && row < J.rows[J.nbox]; row += gridDim.x) {
         int b = 0;
-        while (q >= J.start[b + 1]) ++b;
+        while (row >= J.rows[b + 1]) ++b;
         const int *x = J.box[b];
-        const long long r = q - J.start[b];
+        const int rl = row - J.rows[b];
         const int nj = x[3] - x[2], nk = x[5] - x[4];
-        int i, j, k;
-        if (nk > 1) {  // rows along k: coalesced
-            k = x[4] + (int)(r % nk);
-            const long long t = r / nk;
-            j = x[2] + (int)(t % nj);
-            i = x[0] + (int)(t / nj);
-        } else {       // a z column: run along j
-            k = x[4];
-            j = x[2] + (int)(r % nj);
-            i = x[0] + (int)(r / nj);
-        }
-        const size_t c = g.at(i, j, k);
-        // Coherent (not .nc) loads: ghost cells were stored by a peer GPU
-        // while this kernel may already have been running; the flag acquire
-        // above (observed through the barrier) orders these loads after them.
-        const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy], cur[c - 1],
-                                   cur[c + 1]));
-        nxt[c] = v;
-        if (res) worst = fmax(worst, fabs(__dsub_rn(v, cur[c])));
-        const int coord[3] = {i, j, k};
+        const bool along_k = nk > 1;
+        const int i = x[0] + (along_k ? rl / nj : rl);
+        const int j = along_k ? x[2] + rl % nj : x[2];
+        const int len = along_k ? nk : nj;
+        const size_t c0 = g.at(i, j, x[4]);
+        const size_t step_c = along_k ? 1 : sy;
+        // neighbour-facing planes this whole row lies on (x and y faces; a
+        // z face is one k of a k-row, or every cell of a z column)
+        unsigned whole = 0, zface = 0;
 #pragma unroll
-        for (int d = 0; d < 6; ++d)
-            if (J.remote[d] && coord[d >> 1] == J.face[d]) J.remote[d][(long long)c + J.shift[d]] = v;
+        for (int d = 0; d < 6; ++d) {
+            if (!J.remote[d]) continue;
+            if (d < 2 ? i == J.face[d] : d < 4 ? (along_k ? j == J.face[d] : false) : false)
+                whole |= 1u << d;
+            if (d >= 4 || (d >= 2 && !along_k)) zface |= 1u << d;
+        }
+#pragma unroll 2
+        for (int t = threadIdx.x; t < len; t += blockDim.x) {
+            const size_t c = c0 + (size_t)t * step_c;
+            // Coherent (not .nc) loads: ghost cells were stored by a peer
+            // GPU while this kernel may already have been running; the flag
+            // acquire above (observed through the barrier) orders the loads.
+            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy],
+                                       cur[c - 1], cur[c + 1]));
+            nxt[c] = v;
+            if (res) worst = fmax(worst, fabs(__dsub_rn(v, cur[c])));
+            unsigned on = whole;
+            if (zface) {
+                const int jj = along_k ? j : j + t, kk = along_k ? x[4] + t : x[4];
+#pragma unroll
+                for (int d = 2; d < 6; ++d)
+                    if ((zface >> d) & 1u)
+                        if ((d < 4 ? jj : kk) == J.face[d]) on |= 1u << d;
+            }
+#pragma unroll
+            for (int d = 0; d < 6; ++d)
+                if ((on >> d) & 1u) J.remote[d][(long long)c + J.shift[d]] = v;
+        }
     }
     if (res) warp_max_to_global(worst, res);
     __syncthreads();
@@ -921,26 +936,30 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         J.face[d] = (d & 1) ? ext[d >> 1] : 1;
         J.shift[d] = (d & 1) ? -span[d >> 1] : span[d >> 1];
     }
-    J.start[0] = 0;
+    J.rows[0] = 0;
+    long long n = 0;
     for (int q = 0; q < nbox; ++q) {
         const int *x = boxes + 6 * q;
         if (x[0] < 1 || x[2] < 1 || x[4] < 1 || x[1] > bx + 1 || x[3] > by + 1 || x[5] > bz + 1)
             return HX_E_INVALID;
-        const long long cells = (long long)std::max(0, x[1] - x[0]) * std::max(0, x[3] - x[2]) *
-                                std::max(0, x[5] - x[4]);
+        const int ni = std::max(0, x[1] - x[0]), nj = std::max(0, x[3] - x[2]),
+                  nk = std::max(0, x[5] - x[4]);
+        if ((long long)ni * nj * nk == 0) continue;
         for (int e = 0; e < 6; ++e) J.box[J.nbox][e] = x[e];
-        if (cells == 0) continue;
-        J.start[J.nbox + 1] = J.start[J.nbox] + cells;
+        const long long rows = nk > 1 ? (long long)ni * nj : ni;
+        if (J.rows[J.nbox] + rows > 0x7fffffffLL) return HX_E_INVALID;
+        J.rows[J.nbox + 1] = J.rows[J.nbox] + (int)rows;
+        n += (long long)ni * nj * nk;
         ++J.nbox;
     }
-    const long long n = J.start[J.nbox];
     static int mult = 0;
     if (!mult) {
         const char *e = getenv("HX_SHELL_GRID_MULT");  // CTAs per SM (tuning)
         mult = e && atoi(e) > 0 ? atoi(e) : 2;
     }
     const unsigned grid = (unsigned)std::max<long long>(
-        1, std::min<long long>((n + 255) / 256, (long long)mult * num_sms()));
+        1, std::min<long long>(std::min<long long>((n + 255) / 256, J.rows[J.nbox]),
+                               (long long)mult * num_sms()));
     shell_put_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
         cur, nxt, by, bz, J, wait_value, signal_value, counter, timeout_ns, err, res, step);
     HX_LAUNCH_CHECK();
