@@ -17,6 +17,9 @@ if [ "$ngpu" -ge 4 ]; then
   tr 4 --dims 3072,3072,3072 2> gpurun_out/${tag}_n4_strong.err | grep '^{' > gpurun_out/${tag}_n4_strong.json
 fi
 python bench.py --block 768 --no-cpu-baseline 2> gpurun_out/${tag}_n1_768.err | grep '^{' > gpurun_out/${tag}_n1_768.json
+if [ "$ngpu" -ge 2 ]; then
+  CUDA_VISIBLE_DEVICES=0,1 python tools/run_osu.py --out gpurun_out/${tag}_osu.json > gpurun_out/${tag}_osu.log 2>&1
+fi
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
   --log-file gpurun_out/${tag}_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-e2e \
   --no-cpu-baseline > gpurun_out/${tag}_ncu_launches.log 2>&1
