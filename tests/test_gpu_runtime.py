@@ -500,3 +500,21 @@ def test_fused_graph_replay_matches(pkg, pes, dims, iters):
     want, _ = jacobi_np.sequential(dims, iters)
     assert eng.assemble().tobytes() == want.tobytes()
     eng.close()
+
+
+@pytest.mark.parametrize("dims,pes,policy", [((3, 2, 40), 6, "b200"), ((2, 3, 5), 6, "reference"),
+                                             ((3, 4, 2), 12, "b200")])
+@pytest.mark.parametrize("exchange,overlap", [("p2p", False), ("p2p", True), ("fused", False)])
+def test_halo_engine_one_cell_thick_blocks(pkg, dims, pes, policy, exchange, overlap):
+    """Blocks one or two cells thick: both faces of an axis on the same
+    plane (the shells overlap, interior boxes are empty), every exchange."""
+    from oracle import jacobi_np
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, policy=policy, exchange=exchange,
+                     overlap=overlap)
+    eng.run(7)
+    eng.check_errors()
+    want, _ = jacobi_np.sequential(dims, 7)
+    assert eng.assemble().tobytes() == want.tobytes()
+    eng.close()
