@@ -138,20 +138,22 @@ class HaloBlock:
 
 
 class _Marks:
-    """CUDA event pairs per (name, block) for optional step timing."""
+    """CUDA event pairs per (name, block) for optional step timing. A timing
+    dict holding the key "_only" (a set of names) records just those."""
 
     def __init__(self, timing):
         self.t = timing
+        self.only = timing.get("_only") if timing is not None else None
         self.open = {}
 
     def begin(self, name, b, stream):
-        if self.t is not None:
+        if self.t is not None and (self.only is None or name in self.only):
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             self.open[(name, b.rank)] = e
 
     def end(self, name, b, stream):
-        if self.t is not None:
+        if self.t is not None and (self.only is None or name in self.only):
             e = torch.cuda.Event(enable_timing=True)
             e.record(stream)
             self.t.setdefault(name, []).append((self.open.pop((name, b.rank)), e))
