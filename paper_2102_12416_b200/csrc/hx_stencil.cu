@@ -493,8 +493,10 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
                 whole |= 1u << d;
             if (d >= 4 || (d >= 2 && !along_k)) zface |= 1u << d;
         }
-#pragma unroll 2
-        for (int t = threadIdx.x; t < len; t += blockDim.x) {
+        // One cell: relax, store locally, fold the residual, and store to
+        // every neighbour-facing plane it lies on except `skip` (the row's
+        // primary face when the caller stores that one as a pair).
+        auto cell = [&](int t, unsigned skip) -> double {
             const size_t c = c0 + (size_t)t * step_c;
             // Coherent (not .nc) loads: ghost cells were stored by a peer
             // GPU while this kernel may already have been running; the flag
@@ -503,7 +505,7 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
                                        cur[c - 1], cur[c + 1]));
             nxt[c] = v;
             if (res) worst = fmax(worst, fabs(__dsub_rn(v, cur[c])));
-            unsigned on = whole;
+            unsigned on = whole & ~skip;
             if (zface) {
                 const int jj = along_k ? j : j + t, kk = along_k ? x[4] + t : x[4];
 #pragma unroll
@@ -514,6 +516,29 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
 #pragma unroll
             for (int d = 0; d < 6; ++d)
                 if ((on >> d) & 1u) J.remote[d][(long long)c + J.shift[d]] = v;
+            return v;
+        };
+        if (along_k && whole) {
+            // the row lies on a face: store it to the neighbour in 16-byte
+            // pairs (half the NVLink transactions), pairs aligned on the
+            // neighbour's side
+            const int dp = __ffs(whole) - 1;
+            double *r0 = J.remote[dp] + ((long long)c0 + J.shift[dp]);
+            const int a = (int)(((uintptr_t)r0 >> 3) & 1);  // leading single
+            if (a && threadIdx.x == 0) r0[0] = cell(0, 1u << dp);
+            for (int p = threadIdx.x; a + 2 * p < len; p += blockDim.x) {
+                const int t = a + 2 * p;
+                const double v0 = cell(t, 1u << dp);
+                if (t + 1 < len) {
+                    const double v1 = cell(t + 1, 1u << dp);
+                    *reinterpret_cast<double2 *>(r0 + t) = make_double2(v0, v1);
+                } else {
+                    r0[t] = v0;
+                }
+            }
+        } else {
+#pragma unroll 2
+            for (int t = threadIdx.x; t < len; t += blockDim.x) (void)cell(t, 0u);
         }
     }
     if (res) warp_max_to_global(worst, res);
