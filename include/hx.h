@@ -199,15 +199,19 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
  * address and the receive copies straight out of the sender's buffer over
  * NVLink (one copy, any size below 2^31 bytes), the send completing when
  * the slot comes back. The message index is device state (*seq, one per endpoint,
- * advanced by each launch), so send/recv sequences can be captured in CUDA
- * graphs.
+ * advanced by each launch; for the sender a ticket word: index << 32 | CTAs
+ * of the launch arrived), so send/recv sequences can be captured in CUDA
+ * graphs. Consecutive sends on one stream overlap on the GPU (each claims
+ * its index and slot, then lets the next launch start) and still complete
+ * in stream order; a send after a receive on the same stream waits for it.
  *   send k: wait until *credit >= k+1-depth (slot k % depth free), write
  *           the payload into the slot (a peer-mapped pointer) and its header.
  *   recv k: wait for the header tag, copy min(len, capacity) bytes into dst,
  *           write len to *len_out (nullable; len > capacity = truncated) and
  *           store *credit = k+1 (a peer-mapped pointer).
  * stride must hold 16 + 8 * ceil(min(bytes, HX_CHAN_LL_MAX) / 4) (LL messages).
- * counter: one zero-initialised uint32 per endpoint and direction. Waits
+ * counter: zero-initialised uint32s — `depth` of them for a send (one per
+ * slot), one for a receive — per endpoint and direction. Waits
  * are bounded by timeout_ns (then *err = HX_E_TIMEOUT). */
 #define HX_CHAN_LL_MAX 8192u
 int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int depth,
@@ -217,6 +221,13 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
                  unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
                  unsigned long long *len_out, unsigned long long timeout_ns, int *err,
                  void *stream);
+/* Diagnostics: channel operations launched on `device` afterwards write
+ * %globaltimer stamps — 8 per message, message k at [(k % 256) * 8] — into
+ * send_trace / recv_trace (device buffers of 2048 uint64 — send: 2048 +
+ * 256 * 320, the claimed index + 1 per CTA per launch serial — or null).
+ * send: entry, index+slot claimed, published, pulled (pull mode), done;
+ * recv: entry, predecessor done, header seen, copied. */
+int hx_chan_trace(int device, void *send_trace, void *recv_trace);
 
 /* ---------------------------------------------------------------- flags --
  * Persistent-channel completion words (the Channel API's per-direction

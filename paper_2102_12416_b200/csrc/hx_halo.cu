@@ -17,6 +17,8 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <mutex>
+#include <unordered_map>
 
 #include "hx_internal.cuh"
 
@@ -275,20 +277,38 @@ struct ChanDir {
     unsigned int *counter;           // last-CTA counter (local, zero-initialised)
     unsigned long long stride;
     int depth;
+    unsigned long long *trace;       // diagnostics (hx_chan_trace), usually null
 };
+
+// Diagnostic timestamps (%globaltimer): 8 per message, ring of 256 messages.
+__device__ __forceinline__ void chan_stamp(const ChanDir &c, unsigned long long k, int i) {
+    if (c.trace) c.trace[(k & 255) * 8 + i] = hx::globaltimer();
+}
 
 constexpr unsigned long long CHAN_HDR = 16;      // [header][source pointer (pull)]
 constexpr unsigned long long CHAN_PULL = 1ull << 31;  // header length flag: pull from the source
 
 // True in the CTA that finishes last (after every CTA's copy). A single CTA
 // needs no counter: the barrier orders its threads' stores before thread
-// 0's system-scope release, which is cumulative over them.
-__device__ __forceinline__ bool chan_last_cta(unsigned int *counter) {
+// 0's system-scope release, which is cumulative over them. Otherwise each
+// CTA fences, then counts its arrival; the last CTA's system-scope release
+// (a send's header, a receive's credit) follows every CTA's copy in
+// causality order. `sys_fence` = 0 (the default for both directions): the
+// per-CTA fence is GPU scope — the arrival count is a GPU-scope
+// synchronisation between CTAs of one GPU, and the release that publishes
+// is at system scope and cumulative, so the peer that acquires it sees
+// every CTA's payload. 1: a system fence per CTA (the round-1 form; it
+// stalls each sending CTA for the NVLink write acknowledgements: 320 vs
+// 500 GB/s at 4 MiB). 2: no fence (diagnostics only — unordered).
+__device__ __forceinline__ bool chan_last_cta(unsigned int *counter, int sys_fence = 0) {
     __shared__ bool last;
     __syncthreads();
     if (gridDim.x == 1) return true;
     if (threadIdx.x == 0) {
-        __threadfence_system();  // this CTA's copy, before the count
+        if (sys_fence == 1)
+            __threadfence_system();
+        else if (sys_fence == 0)
+            __threadfence();
         last = atomicAdd(counter, 1u) + 1u == gridDim.x;
         if (last) *counter = 0u;
     }
@@ -321,19 +341,54 @@ __device__ __forceinline__ void store4(unsigned char *p, unsigned v, unsigned lo
     for (unsigned b = 0; b < 4 && b < room; ++b) p[b] = (unsigned char)(v >> (8 * b));
 }
 
+// Message index of this send launch. Every CTA adds one to the ticket word
+// (message index in the high 32 bits, CTAs of the current launch arrived in
+// the low 32); the launch's last CTA rolls it over to the next index. Sends
+// on a stream claim in launch order: a launch starts only after every CTA of
+// its predecessor triggered its dependents, which each does after claiming.
+// The roll-over must be PERFORMED before this CTA triggers its dependents:
+// an atomic whose result is unused compiles to a fire-and-forget RED that
+// can sit behind the SM's queued NVLink stores while a CTA of the next
+// launch claims (measured: launches whose CTAs straddled two indices), so
+// the claim ends with a GPU-scope fence.
+__device__ __forceinline__ unsigned long long chan_claim(unsigned long long *ticket) {
+    const unsigned long long old = atomicAdd(ticket, 1ull);
+    if ((old & 0xffffffffull) + 1 == gridDim.x) atomicAdd(ticket, (1ull << 32) - gridDim.x);
+    __threadfence();
+    return old >> 32;
+}
+
+// A send reads only its source and the channel state, so consecutive sends
+// on one stream may run concurrently (`early`: the host saw that the
+// previous channel operation on this stream was a send, so nothing that
+// triggers early can still be writing the source; any other predecessor
+// kernel triggers at its completion). Send k+1 claims its index and slot,
+// copies and publishes while send k still runs; it waits for its
+// predecessor only at its end, so sends still complete in stream order.
+// Without `early` the send waits for its predecessor first (a preceding
+// receive may be writing the buffer this send reads).
 __global__ void __launch_bounds__(256)
 chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
-                 unsigned long long timeout_ns, int *err) {
+                 unsigned long long timeout_ns, int *err, int flags) {
+    const bool early = flags & 1;
     __shared__ int ok;
     __shared__ unsigned long long k;
-    chan_dependent_prologue();
+    const unsigned long long t_in = c.trace ? hx::globaltimer() : 0;
+    if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
-        k = *(volatile unsigned long long *)c.seq;
+        k = chan_claim(c.seq);
+        if (blockIdx.x == 0 && c.trace) c.trace[(k & 255) * 8] = t_in;
+        // diagnostics: the index each CTA of launch `serial` claimed
+        if (c.trace && blockIdx.x < 320)
+            c.trace[2048 + ((flags >> 8) & 255) * 320 + blockIdx.x] = k + 1;
         // slot k % depth is free once the receiver consumed message k - depth
         ok = k < (unsigned long long)c.depth ||
              hx::spin_until(c.credit, k + 1 - c.depth, timeout_ns, err, 0);
     }
     __syncthreads();
+    if (blockIdx.x == 0 && threadIdx.x == 0) chan_stamp(c, k, 1);
+    // only now may the next send launch: a launch never waits on a later one
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     char *slot = c.slots + (k % c.depth) * c.stride;
     unsigned long long *hdr = reinterpret_cast<unsigned long long *>(slot);
     const unsigned long long tag = (k + 1) & 0xffffffffull;
@@ -345,30 +400,34 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
                 st_relaxed_sys(words + w, (tag << 32) | load4(src + 4 * w, bytes - 4 * w));
             if (threadIdx.x == 0) {
                 st_relaxed_sys(hdr, (tag << 32) | bytes);
-                *c.seq = k + 1;
+                chan_stamp(c, k, 2);
             }
         }
-        return;
-    }
-    if (bytes > HX_CHAN_LL_MAX && CHAN_HDR + bytes > c.stride) {
+    } else if (CHAN_HDR + bytes > c.stride) {
         // does not fit a slot: single CTA publishes the source, waits for the pull
         if (ok && threadIdx.x == 0) {
             st_relaxed_sys(hdr + 1, (unsigned long long)(uintptr_t)src);
             hx::st_release_sys(hdr, (tag << 32) | CHAN_PULL | bytes);  // orders the pointer
+            chan_stamp(c, k, 2);
             // the receiver copies straight out of src over NVLink; src is
             // reusable (the send complete) once it hands the slot back
-            if (hx::spin_until(c.credit, k + 1, timeout_ns, err, 0)) *c.seq = k + 1;
+            hx::spin_until(c.credit, k + 1, timeout_ns, err, 0);
+            chan_stamp(c, k, 3);
         }
-        return;
+    } else {
+        if (ok)
+            copy_bytes(slot + CHAN_HDR, (const char *)src, bytes,
+                       blockIdx.x * (size_t)blockDim.x + threadIdx.x,
+                       (size_t)gridDim.x * blockDim.x, false);
+        // one arrival counter per slot: overlapping sends use different slots
+        // flags bits 1-2: per-CTA fence (chan_last_cta; HX_CHAN_DIAG_FENCE)
+        if (chan_last_cta(c.counter + k % c.depth, (flags >> 1) & 3) && threadIdx.x == 0 && ok) {
+            hx::st_release_sys(hdr, (tag << 32) | bytes);  // orders every CTA's payload
+            chan_stamp(c, k, 2);
+        }
     }
-    if (ok)
-        copy_bytes(slot + CHAN_HDR, (const char *)src, bytes,
-                   blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x,
-                   false);
-    if (chan_last_cta(c.counter) && threadIdx.x == 0 && ok) {
-        hx::st_release_sys(hdr, (tag << 32) | bytes);  // release: orders every CTA's payload
-        *c.seq = k + 1;
-    }
+    if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0) chan_stamp(c, k, 4);
 }
 
 __global__ void __launch_bounds__(256)
@@ -378,9 +437,14 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
     __shared__ bool pull;
     __shared__ unsigned long long k, len;
     __shared__ const char *from;
+    const unsigned long long t_in = c.trace ? hx::globaltimer() : 0;
     chan_dependent_prologue();
     if (threadIdx.x == 0) {
         k = *(volatile unsigned long long *)c.seq;
+        if (blockIdx.x == 0 && c.trace) {
+            c.trace[(k & 255) * 8] = t_in;
+            chan_stamp(c, k, 1);
+        }
         const unsigned long long tag = (k + 1) & 0xffffffffull;
         const unsigned long long *hdr =
             reinterpret_cast<const unsigned long long *>(c.slots + (k % c.depth) * c.stride);
@@ -395,6 +459,7 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                 break;
             }
         }
+        if (blockIdx.x == 0) chan_stamp(c, k, 2);
         pull = (h & CHAN_PULL) != 0;
         len = h & (CHAN_PULL - 1);
         if (ok && len > HX_CHAN_LL_MAX) {
@@ -431,6 +496,7 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                    true);
     }
     if (chan_last_cta(c.counter) && threadIdx.x == 0 && ok) {
+        chan_stamp(c, k, 3);
         if (len_out) *len_out = len;  // > capacity: the caller reports truncation
         // every thread's slot reads fed its stores before the barrier, so
         // the slot may be handed back without a fence
@@ -698,12 +764,20 @@ int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream, 
     return 0;
 }
 
-static unsigned chan_grid(unsigned long long bytes) {
+// Grid of a channel copy: >= 16 KiB per CTA, at most `env` CTAs (default
+// `dflt`; read per call so a sweep can change it inside one process).
+static unsigned chan_grid(unsigned long long bytes, const char *env, unsigned dflt) {
+    const char *e = getenv(env);
+    const unsigned long long cap = e && atoi(e) > 0 ? (unsigned long long)atoi(e) : dflt;
+    const unsigned long long want = (bytes + 16383) / 16384;
+    return (unsigned)std::max<unsigned long long>(1, std::min(want, cap));
+}
+
+static unsigned chan_sms() {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const unsigned long long want = (bytes + 16383) / 16384;  // ~16 KiB per CTA
-    return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, 2ull * sms));
+    return (unsigned)sms;
 }
 
 static cudaLaunchConfig_t chan_launch_config(unsigned grid, void *stream, cudaLaunchAttribute *attr) {
@@ -719,6 +793,34 @@ static cudaLaunchConfig_t chan_launch_config(unsigned grid, void *stream, cudaLa
     return cfg;
 }
 
+// The last channel operation enqueued on each stream (true = a send): a send
+// right after a send may overlap it (chan_send_kernel `early`).
+static std::mutex chan_last_mu;
+static std::unordered_map<void *, bool> chan_last_send;
+
+static unsigned long long *chan_trace_buf[2][64];  // [send / recv][device]
+
+int hx_chan_trace(int device, void *send_trace, void *recv_trace) {
+    if (device < 0 || device >= 64) return HX_E_INVALID;
+    chan_trace_buf[0][device] = (unsigned long long *)send_trace;
+    chan_trace_buf[1][device] = (unsigned long long *)recv_trace;
+    return 0;
+}
+
+static unsigned long long *chan_trace_of(int role) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return dev >= 0 && dev < 64 ? chan_trace_buf[role][dev] : nullptr;
+}
+
+static bool chan_note(void *stream, bool send) {
+    std::lock_guard<std::mutex> lock(chan_last_mu);
+    bool &last = chan_last_send[stream];
+    const bool prev = last;
+    last = send;
+    return prev;
+}
+
 int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int depth,
                  unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
                  unsigned long long timeout_ns, int *err, void *stream) {
@@ -727,12 +829,22 @@ int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int 
     const unsigned long long need =
         CHAN_HDR + (bytes <= HX_CHAN_LL_MAX ? 8 * ((bytes + 3) / 4) : pull ? 0 : bytes);
     if (need > stride || bytes >= CHAN_PULL) return HX_E_INVALID;
-    ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
-    const unsigned grid = (bytes <= HX_CHAN_LL_MAX || pull) ? 1u : chan_grid(bytes);
+    ChanDir c{(char *)slots, credit, seq, counter, stride, depth, chan_trace_of(0)};
+    // sends overlap each other, so each needs few CTAs (HX_CHAN_SEND_CTAS,
+    // default 32: swept 32-296, best at 1-4 MiB; profiles/r1_pchannel.md)
+    const unsigned grid =
+        (bytes <= HX_CHAN_LL_MAX || pull) ? 1u : chan_grid(bytes, "HX_CHAN_SEND_CTAS", 32);
     cudaLaunchAttribute attr;
     const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
+    // per-CTA fence of a bulk send (chan_last_cta): 0 GPU scope (default),
+    // 1 system scope, 2 none (diagnostics) — HX_CHAN_DIAG_FENCE
+    const char *diag = getenv("HX_CHAN_DIAG_FENCE");
+    const int fmode = diag ? (atoi(diag) & 3) : 0;
+    static unsigned serial = 0;  // diagnostics: launch serial (trace claims)
+    const int early = (chan_note(stream, true) ? 1 : 0) | (fmode << 1) |
+                      (int)((serial++ & 255u) << 8);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_send_kernel, c, (const unsigned char *)src,
-                              (unsigned long long)bytes, timeout_ns, err));
+                              (unsigned long long)bytes, timeout_ns, err, early));
     return 0;
 }
 
@@ -742,10 +854,11 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
                  void *stream) {
     if (!slots || !credit || !seq || !counter || depth < 1 || (capacity && !dst))
         return HX_E_INVALID;
-    ChanDir c{(char *)slots, credit, seq, counter, stride, depth};
+    ChanDir c{(char *)slots, credit, seq, counter, stride, depth, chan_trace_of(1)};
+    chan_note(stream, false);
     cudaLaunchAttribute attr;
     // sized by the sink: a pulled message may be far larger than a slot
-    const cudaLaunchConfig_t cfg = chan_launch_config(chan_grid(capacity), stream, &attr);
+    const cudaLaunchConfig_t cfg = chan_launch_config(chan_grid(capacity, "HX_CHAN_RECV_CTAS", 2 * chan_sms()), stream, &attr);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_recv_kernel, c, (unsigned char *)dst,
                               (unsigned long long)capacity, len_out, timeout_ns, err));
     return 0;

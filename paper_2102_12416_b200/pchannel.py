@@ -12,7 +12,9 @@ All of it is allocated and mapped once (NVLink P2P between the two GPUs).
 peer's slot over NVLink and publish its header (tag k + 1 and length in one
 word; up to 8 KiB as LL words that carry the tag themselves, so no fence is
 needed; payloads that fit a slot bulk-copied with the header
-release-stored, so the sender may run ``depth`` messages ahead; larger
+release-stored, so the sender may run ``depth`` messages ahead — and
+consecutive sends on one stream overlap on the GPU, each in its own slot,
+so a stream of them keeps NVLink busy across kernel boundaries; larger
 payloads are not copied by the sender at all: the header publishes the
 source address, the receiver copies straight out of it, and the send
 completes when the slot comes back). ``recv`` is one kernel: wait for the
@@ -66,9 +68,11 @@ class PersistentChannel:
             self._dir.append({
                 "slots": torch.zeros(depth * self.stride, dtype=torch.uint8, device=rdev),
                 "rseq": torch.zeros(1, dtype=torch.int64, device=rdev),
-                "tmeta": torch.zeros(2, dtype=torch.int64, device=tdev),  # credit, seq
+                # credit, ticket (message index << 32 | CTAs of the current launch)
+                "tmeta": torch.zeros(2, dtype=torch.int64, device=tdev),
                 "rctr": torch.zeros(2, dtype=torch.int32, device=rdev),   # counter, err
-                "tctr": torch.zeros(2, dtype=torch.int32, device=tdev),
+                # [_, err, one arrival counter per slot] (overlapping sends)
+                "tctr": torch.zeros(2 + depth, dtype=torch.int32, device=tdev),
                 "lens_out": torch.zeros(tickets, dtype=torch.int64, device=rdev),
                 "posted": 0,
             })
@@ -94,7 +98,7 @@ class PersistentChannel:
         _lib.call("hx_set_device", gpu)
         _lib.call("hx_chan_send", src.data_ptr(), n, d["slots"].data_ptr(), self.stride,
                   self.depth, self._ptr(d["tmeta"]), self._ptr(d["tmeta"], 1),
-                  self._ptr(d["tctr"]), self.timeout_ns, self._ptr(d["tctr"], 1),
+                  self._ptr(d["tctr"], 2), self.timeout_ns, self._ptr(d["tctr"], 1),
                   self._stream(gpu, stream))
 
     def recv(self, end: int, dst: torch.Tensor, capacity: int | None = None, stream=None) -> int:
@@ -136,7 +140,7 @@ class PersistentChannel:
         """Per direction: (sent, received) message counts (device state)."""
         out = []
         for d in self._dir:
-            out.append((int(d["tmeta"][1].item()), int(d["rseq"][0].item())))
+            out.append((int(d["tmeta"][1].item()) >> 32, int(d["rseq"][0].item())))
         return out
 
     def close(self) -> None:

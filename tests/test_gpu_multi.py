@@ -215,3 +215,45 @@ def test_osu_cli_channel_benchmarks(cuda, tmp_path):
     assert len(rows) == 3 and rows[1].startswith("channel-latency")
     assert main(["--benchmark", "channel-bandwidth", "--sizes", "65536", "--window", "8",
                  "--iters", "2"]) == 0
+
+
+@needs2
+@pytest.mark.parametrize("depth", [1, 4])
+def test_persistent_channel_send_bursts_overlap(cuda, depth):
+    """Back-to-back sends on one stream overlap on the GPU (each claims its
+    index and slot, then lets the next launch start). A burst of 48 sends
+    of mixed sizes — LL, slot-sized bulk and pulled — with one source
+    tensor rewritten by ordinary kernels between some of them, then the
+    matching receives: every payload arrives in order and equals the
+    source as it was when its send was enqueued."""
+    from paper_2102_12416_b200.completion import OK
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    rng = np.random.default_rng(100 + depth)
+    slot = 1 << 18
+    ch = PersistentChannel(0, 1, slot_bytes=slot, depth=depth, timeout_s=20)
+    s0, s1 = torch.cuda.Stream(device=0), torch.cuda.Stream(device=1)
+    sizes = [int(x) for x in rng.choice([8, 5000, 8193, 100000, slot, slot + 1, 3 << 20], 48)]
+    big = max(sizes)
+    shared = torch.zeros(big, dtype=torch.uint8, device="cuda:0")
+    want, srcs = [], []
+    for k, n in enumerate(sizes):
+        if k % 3 == 0:  # an ordinary kernel rewrites the shared source before this send
+            srcs.append(shared)
+            want.append(np.full(n, k % 251, dtype=np.uint8))
+        else:
+            m = rng.integers(0, 256, n, dtype=np.uint8)
+            srcs.append(torch.from_numpy(m).to("cuda:0"))
+            want.append(m)
+    for k, n in enumerate(sizes):
+        if k % 3 == 0:
+            with torch.cuda.stream(s0):
+                shared.fill_(k % 251)
+        ch.send(0, srcs[k], n, stream=s0)
+    sinks = [torch.zeros(big, dtype=torch.uint8, device="cuda:1") for _ in sizes]
+    tickets = [ch.recv(1, sink, big, stream=s1) for sink in sinks]
+    ch.check()
+    for k, n in enumerate(sizes):
+        assert ch.completion(1, tickets[k], big) == (OK, n)
+        assert np.array_equal(sinks[k][:n].cpu().numpy(), want[k]), k
+    assert ch.counters[0] == (48, 48)
