@@ -352,6 +352,8 @@ __device__ __forceinline__ void store4(unsigned char *p, unsigned v, unsigned lo
 // launch claims (measured: launches whose CTAs straddled two indices), so
 // the claim ends with a GPU-scope fence.
 __device__ __forceinline__ unsigned long long chan_claim(unsigned long long *ticket) {
+    // one CTA: a single atomic whose result is used — performed, no fence
+    if (gridDim.x == 1) return atomicAdd(ticket, 1ull << 32) >> 32;
     const unsigned long long old = atomicAdd(ticket, 1ull);
     if ((old & 0xffffffffull) + 1 == gridDim.x) atomicAdd(ticket, (1ull << 32) - gridDim.x);
     __threadfence();
@@ -367,7 +369,7 @@ __device__ __forceinline__ unsigned long long chan_claim(unsigned long long *tic
 // predecessor only at its end, so sends still complete in stream order.
 // Without `early` the send waits for its predecessor first (a preceding
 // receive may be writing the buffer this send reads).
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
                  unsigned long long timeout_ns, int *err, int flags) {
     const bool early = flags & 1;
@@ -495,7 +497,10 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                    blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x,
                    true);
     }
-    if (chan_last_cta(c.counter) && threadIdx.x == 0 && ok) {
+    // no fence before the arrival count: a CTA's slot (or source) reads are
+    // complete once the barrier passed — their values fed stores issued
+    // before it — and that is all the credit promises the sender
+    if (chan_last_cta(c.counter, 2) && threadIdx.x == 0 && ok) {
         chan_stamp(c, k, 3);
         if (len_out) *len_out = len;  // > capacity: the caller reports truncation
         // every thread's slot reads fed its stores before the barrier, so
@@ -764,12 +769,13 @@ int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream, 
     return 0;
 }
 
-// Grid of a channel copy: >= 16 KiB per CTA, at most `env` CTAs (default
+// Grid of a channel copy: >= per_cta bytes per CTA, at most `env` CTAs (default
 // `dflt`; read per call so a sweep can change it inside one process).
-static unsigned chan_grid(unsigned long long bytes, const char *env, unsigned dflt) {
+static unsigned chan_grid(unsigned long long bytes, const char *env, unsigned dflt,
+                          unsigned long long per_cta = 16384) {
     const char *e = getenv(env);
     const unsigned long long cap = e && atoi(e) > 0 ? (unsigned long long)atoi(e) : dflt;
-    const unsigned long long want = (bytes + 16383) / 16384;
+    const unsigned long long want = (bytes + per_cta - 1) / per_cta;
     return (unsigned)std::max<unsigned long long>(1, std::min(want, cap));
 }
 
@@ -780,12 +786,13 @@ static unsigned chan_sms() {
     return (unsigned)sms;
 }
 
-static cudaLaunchConfig_t chan_launch_config(unsigned grid, void *stream, cudaLaunchAttribute *attr) {
+static cudaLaunchConfig_t chan_launch_config(unsigned grid, void *stream, cudaLaunchAttribute *attr,
+                                             unsigned threads = 256) {
     attr->id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr->val.programmaticStreamSerializationAllowed = 1;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(threads);
     cfg.dynamicSmemBytes = 0;
     cfg.stream = (cudaStream_t)stream;
     cfg.attrs = attr;
@@ -830,12 +837,18 @@ int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int 
         CHAN_HDR + (bytes <= HX_CHAN_LL_MAX ? 8 * ((bytes + 3) / 4) : pull ? 0 : bytes);
     if (need > stride || bytes >= CHAN_PULL) return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth, chan_trace_of(0)};
-    // sends overlap each other, so each needs few CTAs (HX_CHAN_SEND_CTAS,
-    // default 32: swept 32-296, best at 1-4 MiB; profiles/r1_pchannel.md)
-    const unsigned grid =
-        (bytes <= HX_CHAN_LL_MAX || pull) ? 1u : chan_grid(bytes, "HX_CHAN_SEND_CTAS", 32);
+    // sends overlap each other, so each needs few CTAs: HX_CHAN_SEND_CTAS
+    // (default 64) x HX_CHAN_SEND_THREADS (default 512), swept in
+    // profiles/r1_pchannel.md
+    const unsigned grid = (bytes <= HX_CHAN_LL_MAX || pull)
+                              ? 1u
+                              : chan_grid(bytes, "HX_CHAN_SEND_CTAS", 64, 32768);
     cudaLaunchAttribute attr;
-    const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
+    // each thread keeps 4 x 16 B of stores in flight per iteration
+    const char *te = getenv("HX_CHAN_SEND_THREADS");
+    const int tw = te ? atoi(te) : 512;
+    const unsigned threads = grid > 1 && (tw == 512 || tw == 1024) ? (unsigned)tw : 256u;
+    const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr, threads);
     // per-CTA fence of a bulk send (chan_last_cta): 0 GPU scope (default),
     // 1 system scope, 2 none (diagnostics) — HX_CHAN_DIAG_FENCE
     const char *diag = getenv("HX_CHAN_DIAG_FENCE");
@@ -858,7 +871,8 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
     chan_note(stream, false);
     cudaLaunchAttribute attr;
     // sized by the sink: a pulled message may be far larger than a slot
-    const cudaLaunchConfig_t cfg = chan_launch_config(chan_grid(capacity, "HX_CHAN_RECV_CTAS", 2 * chan_sms()), stream, &attr);
+    const unsigned grid = chan_grid(capacity, "HX_CHAN_RECV_CTAS", 2 * chan_sms());
+    const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_recv_kernel, c, (unsigned char *)dst,
                               (unsigned long long)capacity, len_out, timeout_ns, err));
     return 0;

@@ -1,6 +1,8 @@
-"""Sweep the persistent channel's copy grids (HX_CHAN_SEND_CTAS,
-HX_CHAN_RECV_CTAS) for the 64-message window bandwidth; one JSON line each.
-usage: pchan_knobs.py SEND_LIST RECV_LIST SIZE_LIST"""
+"""Sweep the persistent channel's copy shapes for the 64-message window
+bandwidth; one JSON line each.
+usage: pchan_knobs.py SEND_CTAS SEND_THREADS SIZES [RECV_THREADS]
+(comma lists; HX_CHAN_SEND_CTAS, HX_CHAN_SEND_THREADS, HX_CHAN_RECV_THREADS)"""
+import itertools
 import json
 import os
 import sys
@@ -8,14 +10,18 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2102_12416_b200.osu import channel_bandwidth  # noqa: E402
 
-sends = sys.argv[1].split(",") if len(sys.argv) > 1 else ["32", "64", "128"]
-recvs = sys.argv[2].split(",") if len(sys.argv) > 2 else ["296"]
-sizes = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1 << 20, 4 << 20, 16 << 20]
-for sc in sends:
-    os.environ["HX_CHAN_SEND_CTAS"] = sc
-    for rc in recvs:
-        os.environ["HX_CHAN_RECV_CTAS"] = rc
-        for size in sizes:
-            r = channel_bandwidth(size, window=64, iters=5, depth=8)
-            print(json.dumps({"send_ctas": sc, "recv_ctas": rc, "size": size,
-                              "gbps": round(r["value_gbps"], 1), "ok": r["verified"]}), flush=True)
+
+def arg(i, dflt):
+    return sys.argv[i].split(",") if len(sys.argv) > i else dflt
+
+
+ctas = arg(1, ["32"])
+threads = arg(2, ["256"])
+sizes = [int(x) for x in arg(3, [str(1 << 20), str(4 << 20), str(16 << 20)])]
+recv_threads = arg(4, ["256"])
+for c, t, rt in itertools.product(ctas, threads, recv_threads):
+    os.environ.update(HX_CHAN_SEND_CTAS=c, HX_CHAN_SEND_THREADS=t, HX_CHAN_RECV_THREADS=rt)
+    for size in sizes:
+        r = channel_bandwidth(size, window=64, iters=5, depth=8)
+        print(json.dumps({"send_ctas": c, "threads": t, "recv_threads": rt, "size": size,
+                          "gbps": round(r["value_gbps"], 1), "ok": r["verified"]}), flush=True)
