@@ -189,7 +189,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper
  * §3.2.2) in its pre-registered device form. One direction is a ring of
  * `depth` slots (`stride` bytes apart) in the receiver's HBM and a credit
- * counter on the sender; a slot holds a 16-byte header — tag k+1 in the high
+ * counter on the sender; a slot holds a 128-byte header block — tag k+1 in the high
  * 32 bits and the length in the low 32, i.e. the arrival flag and the length
  * in one word — then the payload. Payloads up to HX_CHAN_LL_MAX bytes go as
  * LL words (8-byte stores of 4 data bytes + the tag: no fences, the receiver
@@ -209,11 +209,13 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
  *   recv k: wait for the header tag, copy min(len, capacity) bytes into dst,
  *           write len to *len_out (nullable; len > capacity = truncated) and
  *           store *credit = k+1 (a peer-mapped pointer).
- * stride must hold 16 + 8 * ceil(min(bytes, HX_CHAN_LL_MAX) / 4) (LL messages).
+ * stride must hold HX_CHAN_HDR + 8 * ceil(min(bytes, HX_CHAN_LL_MAX) / 4) (LL
+ * messages); the payload starts HX_CHAN_HDR bytes into the slot.
  * counter: zero-initialised uint32s — `depth` of them for a send (one per
  * slot), one for a receive — per endpoint and direction. Waits
  * are bounded by timeout_ns (then *err = HX_E_TIMEOUT). */
 #define HX_CHAN_LL_MAX 8192u
+#define HX_CHAN_HDR 128u
 int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int depth,
                  unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
                  unsigned long long timeout_ns, int *err, void *stream);

@@ -285,7 +285,10 @@ __device__ __forceinline__ void chan_stamp(const ChanDir &c, unsigned long long 
     if (c.trace) c.trace[(k & 255) * 8 + i] = hx::globaltimer();
 }
 
-constexpr unsigned long long CHAN_HDR = 16;      // [header][source pointer (pull)]
+// [header][source pointer (pull)][pad]: the payload starts 128-byte aligned,
+// so a bulk send writes whole lines over NVLink (a 16-byte header put every
+// line of a payload across two; profiles/r1_pchannel.md)
+constexpr unsigned long long CHAN_HDR = HX_CHAN_HDR;
 constexpr unsigned long long CHAN_PULL = 1ull << 31;  // header length flag: pull from the source
 
 // True in the CTA that finishes last (after every CTA's copy). A single CTA
@@ -428,7 +431,12 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
             chan_stamp(c, k, 2);
         }
     }
-    if (early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // Completion order: the launch completes only when every CTA exited, so
+    // CTA 0 alone waiting for the predecessor keeps sends completing in
+    // stream order, while the other CTAs exit at once and free their SM
+    // slots for the next overlapping send (512-thread CTAs at 64 registers:
+    // 2 per SM, so waiting CTAs capped the overlap at about 4 sends).
+    if (early && blockIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (blockIdx.x == 0 && threadIdx.x == 0) chan_stamp(c, k, 4);
 }
 

@@ -38,6 +38,7 @@ from . import _lib
 from .completion import OK, TRUNCATED
 
 LL_MAX = 8192  # include/hx.h HX_CHAN_LL_MAX: payloads up to this go as LL words
+HDR = 128      # include/hx.h HX_CHAN_HDR: header block; the payload is 128-byte aligned
 
 
 class PersistentChannel:
@@ -58,9 +59,9 @@ class PersistentChannel:
         self.timeout_ns = int(timeout_s * 1e9)
         _lib.call("hx_enable_peer", gpu_a, gpu_b)
         _lib.call("hx_enable_peer", gpu_b, gpu_a)
-        # a slot: 16-byte header, then the payload (LL words are 2x the bytes)
+        # a slot: header block, then the payload (LL words are 2x the bytes)
         ll = min(slot_bytes, LL_MAX)
-        self.stride = -(-(16 + max(slot_bytes, 8 * (-(-ll // 4)))) // 256) * 256
+        self.stride = -(-(HDR + max(slot_bytes, 8 * (-(-ll // 4)))) // 256) * 256
         self._dir = []
         for d in (0, 1):  # direction d: endpoint d sends, endpoint 1 - d receives
             tx, rx = self.gpus[d], self.gpus[1 - d]
