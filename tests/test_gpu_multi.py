@@ -257,3 +257,52 @@ def test_persistent_channel_send_bursts_overlap(cuda, depth):
         assert ch.completion(1, tickets[k], big) == (OK, n)
         assert np.array_equal(sinks[k][:n].cpu().numpy(), want[k]), k
     assert ch.counters[0] == (48, 48)
+
+
+@needs2
+def test_persistent_channel_overlapping_claims_are_ordered(cuda):
+    """Overlapping bulk sends claim message indices in launch order: with
+    hx_chan_trace on, every CTA of a launch records the index it claimed,
+    and no launch may straddle two indices (the fire-and-forget roll-over
+    race, profiles/r1_pchannel.md). Large messages and a deep ring make
+    the sends overlap most; payloads must arrive intact."""
+    from paper_2102_12416_b200 import _lib
+    from paper_2102_12416_b200.osu import _graph_pair, _replay_pair
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    size, window = 8 << 20, 24
+    tr = [torch.zeros(2048 + 256 * 320, dtype=torch.int64, device=f"cuda:{g}") for g in (0, 1)]
+    for g in (0, 1):
+        _lib.call("hx_chan_trace", g, tr[g].data_ptr(), None)
+    try:
+        ch = PersistentChannel(0, 1, slot_bytes=size, depth=8, timeout_s=5)
+        src = torch.randint(0, 255, (size,), dtype=torch.uint8, device="cuda:0")
+        sink = torch.zeros(size, dtype=torch.uint8, device="cuda:1")
+        ack = [torch.zeros(8, dtype=torch.uint8, device=f"cuda:{g}") for g in (0, 1)]
+
+        def sender(s):
+            for _ in range(window):
+                ch.send(0, src, size, stream=s)
+            ch.recv(0, ack[0], 8, stream=s)
+
+        def drainer(s):
+            for _ in range(window):
+                ch.recv(1, sink, size, stream=s)
+            ch.send(1, ack[1], 8, stream=s)
+
+        graphs, streams = _graph_pair((0, 1), sender, drainer)
+        _replay_pair((0, 1), graphs, streams, 3)
+        ch.check()
+        assert ch.counters == [(3 * window, 3 * window), (3, 3)]
+        assert torch.equal(sink.cpu(), src.cpu())
+    finally:
+        for g in (0, 1):
+            _lib.call("hx_chan_trace", g, None, None)
+    claims = tr[0][2048:].cpu().numpy().reshape(256, 320)
+    seen = 0
+    for row in claims:
+        v = row[row > 0]
+        if v.size:
+            seen += 1
+            assert v.min() == v.max(), f"one launch claimed indices {sorted(set(v - 1))}"
+    assert seen >= window

@@ -42,6 +42,9 @@ def main():
         rows.append(r)
         print(json.dumps(r), flush=True)
 
+    if ngpu >= 2:  # untimed warm-up: the first graph replays of a process run slow
+        channel_latency(8, iters=500, warmup=50)
+        device_latency(8, iters=500, warmup=50)
     for size in sizes:
         lat_iters = 200 if size <= 65536 else 50
         for api in ("charm-channel", "charm-messaging", "mpi"):
