@@ -372,6 +372,8 @@ __device__ __forceinline__ unsigned long long chan_claim(unsigned long long *tic
 // predecessor only at its end, so sends still complete in stream order.
 // Without `early` the send waits for its predecessor first (a preceding
 // receive may be writing the buffer this send reads).
+// flags: bit 0 early; bits 1-2 per-CTA fence mode of a bulk send
+// (chan_last_cta); bits 8-15 the launch serial (diagnostics, hx_chan_trace).
 __global__ void __launch_bounds__(1024)
 chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
                  unsigned long long timeout_ns, int *err, int flags) {
