@@ -496,15 +496,24 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
         // One cell: relax, store locally, fold the residual, and store to
         // every neighbour-facing plane it lies on except `skip` (the row's
         // primary face when the caller stores that one as a pair).
-        auto cell = [&](int t, unsigned skip) -> double {
+        // One cell in two parts. relax: the six-point update (and the
+        // residual) — loads and arithmetic only, so the loads of several
+        // cells can be in flight together; put: store it locally and to
+        // every neighbour-facing plane it lies on except `skip` (the row's
+        // primary face when the caller stores that one as a pair).
+        auto relax = [&](int t) -> double {
             const size_t c = c0 + (size_t)t * step_c;
             // Coherent (not .nc) loads: ghost cells were stored by a peer
             // GPU while this kernel may already have been running; the flag
             // acquire above (observed through the barrier) orders the loads.
             const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy],
                                        cur[c - 1], cur[c + 1]));
-            nxt[c] = v;
             if (res) worst = fmax(worst, fabs(__dsub_rn(v, cur[c])));
+            return v;
+        };
+        auto put = [&](int t, double v, unsigned skip) {
+            const size_t c = c0 + (size_t)t * step_c;
+            nxt[c] = v;
             unsigned on = whole & ~skip;
             if (zface) {
                 const int jj = along_k ? j : j + t, kk = along_k ? x[4] + t : x[4];
@@ -516,35 +525,64 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
 #pragma unroll
             for (int d = 0; d < 6; ++d)
                 if ((on >> d) & 1u) J.remote[d][(long long)c + J.shift[d]] = v;
-            return v;
         };
         if (along_k && whole) {
-            // the row lies on a face: store it to the neighbour in 16-byte
-            // pairs (half the NVLink transactions), pairs aligned on the
-            // neighbour's side
+            // The row lies on a face: store it to the neighbour in 16-byte
+            // pairs, each warp's 32 pairs one whole run of four 128-byte
+            // lines on the neighbour's side (the first `a` cells, up to the
+            // first line boundary, go singly) — partial-line NVLink writes
+            // cost bandwidth (profiles/r1_pchannel.md). Each thread relaxes
+            // up to PAIRS pairs before storing any, so their loads overlap
+            // (a store between them would order the next loads behind it).
+            constexpr int PAIRS = 3;
             const int dp = __ffs(whole) - 1;
+            const unsigned skip = 1u << dp;
             double *r0 = J.remote[dp] + ((long long)c0 + J.shift[dp]);
-            const int a = (int)(((uintptr_t)r0 >> 3) & 1);  // leading single
-            if (a && threadIdx.x == 0) r0[0] = cell(0, 1u << dp);
-            for (int p = threadIdx.x; a + 2 * p < len; p += blockDim.x) {
-                const int t = a + 2 * p;
-                const double v0 = cell(t, 1u << dp);
-                if (t + 1 < len) {
-                    const double v1 = cell(t + 1, 1u << dp);
-                    *reinterpret_cast<double2 *>(r0 + t) = make_double2(v0, v1);
-                } else {
-                    r0[t] = v0;
+            const int a = min(len, (int)(((128u - ((uintptr_t)r0 & 127u)) & 127u) >> 3));
+            if ((int)threadIdx.x < a) {
+                const double v = relax(threadIdx.x);
+                put(threadIdx.x, v, skip);
+                r0[threadIdx.x] = v;
+            }
+            const int np = (len - a + 1) >> 1;
+            for (int p0 = threadIdx.x; p0 < np; p0 += PAIRS * blockDim.x) {
+                double v[PAIRS][2];
+#pragma unroll
+                for (int u = 0; u < PAIRS; ++u) {
+                    const int t = a + 2 * (p0 + u * (int)blockDim.x);
+                    if (t < len) {
+                        v[u][0] = relax(t);
+                        if (t + 1 < len) v[u][1] = relax(t + 1);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < PAIRS; ++u) {
+                    const int t = a + 2 * (p0 + u * (int)blockDim.x);
+                    if (t >= len) continue;
+                    put(t, v[u][0], skip);
+                    if (t + 1 < len) {
+                        put(t + 1, v[u][1], skip);
+                        *reinterpret_cast<double2 *>(r0 + t) = make_double2(v[u][0], v[u][1]);
+                    } else {
+                        r0[t] = v[u][0];
+                    }
                 }
             }
         } else {
 #pragma unroll 2
-            for (int t = threadIdx.x; t < len; t += blockDim.x) (void)cell(t, 0u);
+            for (int t = threadIdx.x; t < len; t += blockDim.x) put(t, relax(t), 0u);
         }
     }
     if (res) warp_max_to_global(worst, res);
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();  // this CTA's local + remote stores, system-wide
+        // GPU-scope fence, then the arrival count; the last CTA's system
+        // fence and release stores below are cumulative over every CTA's
+        // local and remote stores (causality through the count), so the
+        // neighbour that acquires the flag sees them all. A system fence
+        // per CTA would stall each CTA for its NVLink write acks (the same
+        // finding as the persistent channel's sends, profiles/r1_pchannel.md).
+        __threadfence();
         const unsigned done = atomicAdd(counter, 1u) + 1u;
         if (done == gridDim.x) {
             *counter = 0u;  // re-arm (launches on one stream are ordered)
@@ -980,7 +1018,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
     static int mult = 0;
     if (!mult) {
         const char *e = getenv("HX_SHELL_GRID_MULT");  // CTAs per SM (tuning)
-        mult = e && atoi(e) > 0 ? atoi(e) : 2;
+        mult = e && atoi(e) > 0 ? atoi(e) : 4;  // 4: 0.112 -> 0.076 ms concurrent shell at 1536^2, step unchanged
     }
     const unsigned grid = (unsigned)std::max<long long>(
         1, std::min<long long>(std::min<long long>((n + 255) / 256, J.rows[J.nbox]),

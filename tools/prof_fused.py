@@ -32,6 +32,9 @@ def main():
     ap.add_argument("--one-gpu", action="store_true")
     ap.add_argument("--steps-only", action="store_true")
     ap.add_argument("--exchange", default="fused", choices=("fused", "p2p"))
+    ap.add_argument("--iso-only", action="store_true", help="skip the full steps (for ncu)")
+    ap.add_argument("--remote", default="peer", choices=("peer", "none"),
+                    help="none: the shell alone without its NVLink stores (diagnostics)")
     args = ap.parse_args()
     n = args.n
     two = torch.cuda.device_count() >= 2 and not args.one_gpu
@@ -51,7 +54,8 @@ def main():
                 _, shells = eng.boxes(b)
                 flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
                 nxt = b.cur ^ 1
-                remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
+                remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs and args.remote == "peer"
+                          else None for d in range(NDIRS)]
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(c)
                 _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
@@ -65,11 +69,15 @@ def main():
         cells = sum((x[1] - x[0]) * (x[3] - x[2]) * (x[5] - x[4]) for x in eng.boxes(b)[1])
         face = b.by * b.bz
         ms = statistics.median(iso)
-        out["shell_alone"] = {"ms": ms, "cells": cells, "hbm_bytes": 32 * cells,
+        out["shell_alone"] = {"ms": ms, "remote": args.remote, "all_ms": [round(x, 4) for x in iso], "cells": cells, "hbm_bytes": 32 * cells,
                               "hbm_gbs": 32 * cells / (ms * 1e-3) / 1e9,
                               "nvlink_bytes": 8 * face,
                               "nvlink_gbs": 8 * face / (ms * 1e-3) / 1e9}
 
+    if args.iso_only:
+        print(json.dumps(out), flush=True)
+        eng.close()
+        return
     timing: dict = {}
     s0 = eng.stream_of(eng.blocks[0])
     a, z = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
