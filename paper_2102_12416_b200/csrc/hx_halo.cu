@@ -135,9 +135,11 @@ face_copy_kernel(FaceBatch b) {
 }
 
 // Fused pack + put + signal. Each CTA stores its units, then (after a CTA
-// barrier) thread 0 issues one system-scope fence — cumulative over the
-// barrier, so it covers every thread's peer stores — and bumps the batch
-// counter; the last CTA fences again and release-stores every face's flag.
+// barrier) thread 0 issues a GPU-scope fence and bumps the batch counter;
+// the last CTA fences at system scope and release-stores every face's flag
+// — cumulative, through the count and the barriers, over every CTA's peer
+// stores (a system fence per CTA only stalls each CTA for its NVLink write
+// acknowledgements; profiles/r1_pchannel.md).
 __global__ void __launch_bounds__(FACE_THREADS)
 pack_put_kernel(FaceBatch b, unsigned long long value, unsigned int *counters) {
     for (int unit = blockIdx.x; unit < b.total_blocks; unit += gridDim.x) {
@@ -147,7 +149,7 @@ pack_put_kernel(FaceBatch b, unsigned long long value, unsigned int *counters) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence_system();
+        __threadfence();
         const unsigned done = atomicAdd(&counters[0], 1u) + 1u;
         if (done == gridDim.x) {
             counters[0] = 0u;  // re-arm for the next launch (stream ordered)
