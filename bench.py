@@ -199,6 +199,7 @@ def main() -> int:
     ap.add_argument("--ref-seconds", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-p2p", action="store_true", help="skip the GPU 0 <-> 1 OSU probe")
     ap.add_argument("--policy", choices=("b200", "reference"), default="b200",
                     help="block decomposition: reference = cl/jacobi3d.py:62-76 exactly; b200 = "
                          "same face area, ties broken away from splitting z (strided faces)")
@@ -372,11 +373,50 @@ def main() -> int:
             "cpu_baseline": cpu,
             "e2e": e2e,
         }
-        print(json.dumps(line), flush=True)
     eng.close()
     if world > 1:
         dist.destroy_process_group()
+    if rank == 0:
+        # after the other ranks are done with the GPUs: the metric's "p2p
+        # halo GB/s & 8B latency" between GPUs 0 and 1 (untimed by the step)
+        line["p2p"] = None if args.no_p2p else p2p_probe()
+        print(json.dumps(line), flush=True)
     return 0
+
+
+def p2p_probe() -> dict | None:
+    """OSU-style point to point between GPUs 0 and 1 (configs[1]): 8-byte
+    one-way latency and 4 MiB window bandwidth, device level (one kernel
+    per side: LL ping-pong; pull window) and through the pre-registered
+    persistent channel (graph-replayed send/recv). None on a 1-GPU box."""
+    import torch
+
+    if torch.cuda.device_count() < 2:
+        return None
+    if os.environ.get("CUDA_INJECTION64_PATH"):
+        # under ncu / a tool: kernels are serialised, and the two sides of a
+        # ping-pong must run concurrently on different GPUs
+        return {"skipped": "profiler attached (kernels serialised)"}
+    from paper_2102_12416_b200 import osu
+
+    try:
+        osu.device_latency(8, iters=500, warmup=50)  # warm-up (clocks, first replays)
+        osu.channel_latency(8, iters=200, warmup=20)
+        lat = osu.device_latency(8, iters=2000, warmup=200)
+        bw = osu.device_bandwidth(4 << 20, window=64, iters=5, engine="sm-pull-window")
+        clat = osu.channel_latency(8, iters=1000, warmup=50)
+        cbw = osu.channel_bandwidth(4 << 20, window=64, iters=5)
+    except Exception as e:  # the Jacobi line stands on its own
+        return {"error": f"{type(e).__name__}: {e}"}
+    return {"gpus": [0, 1], "nvlink_peak_gbs": NVLINK_GBS,
+            "latency_8B_us": {"device_ll": lat["value_ns"] / 1e3,
+                              "persistent_channel": clat["value_ns"] / 1e3},
+            "bandwidth_4MiB_gbs": {"device_pull_window": bw["value_gbps"],
+                                   "persistent_channel": cbw["value_gbps"]},
+            "frac_of_nvlink_4MiB": {"device_pull_window": bw["value_gbps"] / NVLINK_GBS,
+                                    "persistent_channel": cbw["value_gbps"] / NVLINK_GBS},
+            "verified": all(r["verified"] for r in (lat, bw, clat, cbw)),
+            "tool": "paper_2102_12416_b200.osu (tools/run_osu.py has the full 8 B-4 MiB sweep)"}
 
 
 def run_e2e(eng, b, args, world, barrier, max_over_ranks, total_cells):

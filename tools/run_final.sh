@@ -21,7 +21,7 @@ if [ "$ngpu" -ge 2 ]; then
   CUDA_VISIBLE_DEVICES=0,1 python tools/run_osu.py --out gpurun_out/${tag}_osu.json > gpurun_out/${tag}_osu.log 2>&1
 fi
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
-  --log-file gpurun_out/${tag}_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-e2e \
+  --log-file gpurun_out/${tag}_launches_n1.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-p2p \
   --no-cpu-baseline > gpurun_out/${tag}_ncu_launches.log 2>&1
 for f in gpurun_out/${tag}_*.json; do
   python -c "
