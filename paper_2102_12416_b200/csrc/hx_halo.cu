@@ -17,6 +17,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <atomic>
 #include <mutex>
 #include <unordered_map>
 
@@ -781,14 +782,40 @@ int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream, 
     return 0;
 }
 
-// Grid of a channel copy: >= per_cta bytes per CTA, at most `env` CTAs (default
-// `dflt`; read per call so a sweep can change it inside one process).
-static unsigned chan_grid(unsigned long long bytes, const char *env, unsigned dflt,
-                          unsigned long long per_cta = 16384) {
-    const char *e = getenv(env);
-    const unsigned long long cap = e && atoi(e) > 0 ? (unsigned long long)atoi(e) : dflt;
+// Channel launch shapes, read once from the environment (tuning and
+// diagnostics; tools/pchan_knobs.py sweeps them one process per setting).
+// Sends overlap each other, so each needs few CTAs: HX_CHAN_SEND_CTAS
+// (default 64) x HX_CHAN_SEND_THREADS (256 / 512 / 1024, default 512);
+// receives HX_CHAN_RECV_CTAS (default 2 x SMs) x 256. HX_CHAN_DIAG_FENCE:
+// the per-CTA fence of a bulk send (chan_last_cta): 0 GPU scope (default),
+// 1 system scope, 2 none (diagnostics only). profiles/r1_pchannel.md.
+struct ChanKnobs {
+    unsigned send_ctas, send_threads, recv_ctas;  // recv_ctas 0: 2 x SMs
+    int fence;
+};
+
+static const ChanKnobs &chan_knobs() {
+    static const ChanKnobs k = [] {
+        auto num = [](const char *name, int dflt) {
+            const char *e = getenv(name);
+            return e && atoi(e) > 0 ? atoi(e) : dflt;
+        };
+        ChanKnobs v;
+        v.send_ctas = (unsigned)num("HX_CHAN_SEND_CTAS", 64);
+        const int t = num("HX_CHAN_SEND_THREADS", 512);
+        v.send_threads = (t == 256 || t == 512 || t == 1024) ? (unsigned)t : 512u;
+        v.recv_ctas = (unsigned)num("HX_CHAN_RECV_CTAS", 0);
+        const char *f = getenv("HX_CHAN_DIAG_FENCE");
+        v.fence = f ? (atoi(f) & 3) : 0;
+        return v;
+    }();
+    return k;
+}
+
+// Grid of a channel copy: >= per_cta bytes per CTA, at most `cap` CTAs.
+static unsigned chan_grid(unsigned long long bytes, unsigned cap, unsigned long long per_cta) {
     const unsigned long long want = (bytes + per_cta - 1) / per_cta;
-    return (unsigned)std::max<unsigned long long>(1, std::min(want, cap));
+    return (unsigned)std::max<unsigned long long>(1, std::min<unsigned long long>(want, cap));
 }
 
 static unsigned chan_sms() {
@@ -849,23 +876,15 @@ int hx_chan_send(const void *src, size_t bytes, void *slots, size_t stride, int 
         CHAN_HDR + (bytes <= HX_CHAN_LL_MAX ? 8 * ((bytes + 3) / 4) : pull ? 0 : bytes);
     if (need > stride || bytes >= CHAN_PULL) return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth, chan_trace_of(0)};
-    // sends overlap each other, so each needs few CTAs: HX_CHAN_SEND_CTAS
-    // (default 64) x HX_CHAN_SEND_THREADS (default 512), swept in
-    // profiles/r1_pchannel.md
-    const unsigned grid = (bytes <= HX_CHAN_LL_MAX || pull)
-                              ? 1u
-                              : chan_grid(bytes, "HX_CHAN_SEND_CTAS", 64, 32768);
-    cudaLaunchAttribute attr;
+    const ChanKnobs &kn = chan_knobs();
+    const bool bulk = bytes > HX_CHAN_LL_MAX && !pull;
     // each thread keeps 4 x 16 B of stores in flight per iteration
-    const char *te = getenv("HX_CHAN_SEND_THREADS");
-    const int tw = te ? atoi(te) : 512;
-    const unsigned threads = grid > 1 && (tw == 512 || tw == 1024) ? (unsigned)tw : 256u;
+    const unsigned grid = bulk ? chan_grid(bytes, kn.send_ctas, 32768) : 1u;
+    const unsigned threads = grid > 1 ? kn.send_threads : 256u;
+    cudaLaunchAttribute attr;
     const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr, threads);
-    // per-CTA fence of a bulk send (chan_last_cta): 0 GPU scope (default),
-    // 1 system scope, 2 none (diagnostics) — HX_CHAN_DIAG_FENCE
-    const char *diag = getenv("HX_CHAN_DIAG_FENCE");
-    const int fmode = diag ? (atoi(diag) & 3) : 0;
-    static unsigned serial = 0;  // diagnostics: launch serial (trace claims)
+    const int fmode = kn.fence;
+    static std::atomic<unsigned> serial{0};  // diagnostics: launch serial (trace claims)
     const int early = (chan_note(stream, true) ? 1 : 0) | (fmode << 1) |
                       (int)((serial++ & 255u) << 8);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_send_kernel, c, (const unsigned char *)src,
@@ -883,7 +902,8 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
     chan_note(stream, false);
     cudaLaunchAttribute attr;
     // sized by the sink: a pulled message may be far larger than a slot
-    const unsigned grid = chan_grid(capacity, "HX_CHAN_RECV_CTAS", 2 * chan_sms());
+    const unsigned cap = chan_knobs().recv_ctas ? chan_knobs().recv_ctas : 2 * chan_sms();
+    const unsigned grid = chan_grid(capacity, cap, 16384);
     const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_recv_kernel, c, (unsigned char *)dst,
                               (unsigned long long)capacity, len_out, timeout_ns, err));

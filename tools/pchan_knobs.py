@@ -1,27 +1,40 @@
-"""Sweep the persistent channel's copy shapes for the 64-message window
-bandwidth; one JSON line each.
-usage: pchan_knobs.py SEND_CTAS SEND_THREADS SIZES [RECV_THREADS]
-(comma lists; HX_CHAN_SEND_CTAS, HX_CHAN_SEND_THREADS, HX_CHAN_RECV_THREADS)"""
+"""Sweep the persistent channel's launch shapes for the 64-message window
+bandwidth; one JSON line per (setting, size). The library reads its knobs
+once per process, so every setting runs in its own subprocess.
+
+usage: pchan_knobs.py SEND_CTAS SEND_THREADS SIZES [RECV_CTAS [FENCE]]
+(comma lists: HX_CHAN_SEND_CTAS, HX_CHAN_SEND_THREADS, message sizes,
+HX_CHAN_RECV_CTAS, HX_CHAN_DIAG_FENCE)"""
 import itertools
 import json
 import os
+import subprocess
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2102_12416_b200.osu import channel_bandwidth  # noqa: E402
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def arg(i, dflt):
     return sys.argv[i].split(",") if len(sys.argv) > i else dflt
 
 
-ctas = arg(1, ["32"])
-threads = arg(2, ["256"])
-sizes = [int(x) for x in arg(3, [str(1 << 20), str(4 << 20), str(16 << 20)])]
-recv_threads = arg(4, ["256"])
-for c, t, rt in itertools.product(ctas, threads, recv_threads):
-    os.environ.update(HX_CHAN_SEND_CTAS=c, HX_CHAN_SEND_THREADS=t, HX_CHAN_RECV_THREADS=rt)
+def child(sizes):
+    sys.path.insert(0, ROOT)
+    from paper_2102_12416_b200.osu import channel_bandwidth
     for size in sizes:
         r = channel_bandwidth(size, window=64, iters=5, depth=8)
-        print(json.dumps({"send_ctas": c, "threads": t, "recv_threads": rt, "size": size,
-                          "gbps": round(r["value_gbps"], 1), "ok": r["verified"]}), flush=True)
+        print(json.dumps({k: os.environ.get(k) for k in KNOBS} |
+                         {"size": size, "gbps": round(r["value_gbps"], 1), "ok": r["verified"]}),
+              flush=True)
+
+
+KNOBS = ("HX_CHAN_SEND_CTAS", "HX_CHAN_SEND_THREADS", "HX_CHAN_RECV_CTAS", "HX_CHAN_DIAG_FENCE")
+
+if __name__ == "__main__":
+    if sys.argv[1:2] == ["--child"]:
+        child([int(x) for x in sys.argv[2].split(",")])
+        sys.exit(0)
+    sizes = arg(3, [str(1 << 20), str(4 << 20), str(16 << 20)])
+    for setting in itertools.product(arg(1, ["64"]), arg(2, ["512"]), arg(4, ["0"]), arg(5, ["0"])):
+        env = dict(os.environ, **dict(zip(KNOBS, setting)))
+        subprocess.run([sys.executable, __file__, "--child", ",".join(sizes)], env=env, check=True)
