@@ -47,8 +47,9 @@ static double sweep(const double *cur, double *nxt, long bx, long by, long bz,
                 t = t / 6.0;
                 o[k] = t;
                 if (want_res) {
+                    /* NaN propagates, as in numpy's max (cl/jacobi3d.py:198) */
                     double dlt = fabs(t - c[k]);
-                    if (dlt > worst) worst = dlt;
+                    if (dlt > worst || dlt != dlt) worst = dlt;
                 }
             }
         }
@@ -87,7 +88,7 @@ static double fan_out(const double *cur, double *nxt, long bx, long by, long bz,
     slab_main(&s[0]);
     for (int q = 0; q < nthreads; ++q) {
         if (q > 0) pthread_join(t[q], NULL);
-        if (s[q].res > worst) worst = s[q].res;
+        if (s[q].res > worst || s[q].res != s[q].res) worst = s[q].res;
     }
     free(s);
     free(t);

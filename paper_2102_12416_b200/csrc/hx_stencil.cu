@@ -104,12 +104,22 @@ __device__ __forceinline__ double sum6(double xm, double xp, double ym, double y
 // word, and an unconditional atomic would serialise at its L2 slice; the max
 // only grows, so lane 0 skips the atomic when the (possibly stale, hence
 // lower) current value already covers its w.
-__device__ __forceinline__ void warp_max_to_global(double worst, unsigned long long *res) {
-    for (int o = 16; o > 0; o >>= 1) worst = fmax(worst, __shfl_xor_sync(0xffffffffu, worst, o));
+// The residual max|nxt - cur| is kept as the bit pattern of |nxt - cur|
+// (sign cleared): for non-negative doubles the unsigned integer order is
+// the numeric order, so the max is an integer max on the integer pipe (no
+// FP64 min/max next to the stencil's own FP64 work), and a NaN difference
+// — whose pattern sorts above +inf — propagates like numpy's max
+// (cl/jacobi3d.py:197-198).
+__device__ __forceinline__ unsigned long long abs_diff_bits(double v, double c) {
+    return (unsigned long long)__double_as_longlong(__dsub_rn(v, c)) & 0x7fffffffffffffffull;
+}
+
+__device__ __forceinline__ void warp_max_to_global(unsigned long long worst,
+                                                   unsigned long long *res) {
+    for (int o = 16; o > 0; o >>= 1) worst = max(worst, __shfl_xor_sync(0xffffffffu, worst, o));
     const int tid = threadIdx.x + blockDim.x * (threadIdx.y + blockDim.y * threadIdx.z);
-    if ((tid & 31) == 0 && worst > 0.0) {
-        const unsigned long long wb = (unsigned long long)__double_as_longlong(worst);
-        if (wb > *(volatile unsigned long long *)res) atomicMax(res, wb);
+    if ((tid & 31) == 0 && worst > 0ull) {
+        if (worst > *(volatile unsigned long long *)res) atomicMax(res, worst);
     }
 }
 
@@ -121,7 +131,8 @@ __device__ __forceinline__ void warp_max_to_global(double worst, unsigned long l
 template <bool RES, int ROWSTEP>
 __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, int soff, int ylo,
                                             int yhi, double (&xm)[PTS], double (&x0)[PTS],
-                                            double *out, int bz, unsigned live, double &worst) {
+                                            double *out, int bz, unsigned live,
+                                            unsigned long long &worst) {
     double v[PTS];
     bool fast = true;
 #pragma unroll
@@ -144,7 +155,7 @@ __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, 
     for (int p = 0; p < PTS; ++p) {
         if (live & (1u << p)) {
             out[(size_t)((p >> 1) * NWARP) * (bz + 2) + 32 * (p & 1)] = v[p];
-            if (RES) worst = fmax(worst, fabs(__dsub_rn(v[p], xm[p])));
+            if (RES) worst = max(worst, abs_diff_bits(v[p], xm[p]));
         }
     }
 }
@@ -216,7 +227,7 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     }
 
     double xm[PTS], x0[PTS];
-    double worst = 0.0;
+    unsigned long long worst = 0;
     int nan_seen = 0;
     {
         const double *s0 = reinterpret_cast<const double *>(smem);
@@ -344,7 +355,7 @@ stencil_pair_kernel(const __grid_constant__ PairMaps maps, double *__restrict__ 
         if (jb + r < j1 && kb + kk < k1) live |= 1u << p;
     }
     double xm[PTS], x0[PTS];
-    double worst = 0.0;
+    unsigned long long worst = 0;
     int nan_seen = 0;
     {
         const double *s0 = reinterpret_cast<const double *>(smem) + shift(rc, ib - 1);
@@ -388,14 +399,14 @@ stencil_generic_kernel(const double *__restrict__ cur, double *__restrict__ nxt,
     const int k = k0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int j = j0 + blockIdx.y * blockDim.y + threadIdx.y;
     const int i = i0 + blockIdx.z;
-    double worst = 0.0;
+    unsigned long long worst = 0;
     if (k < k1 && j < j1) {
         const size_t c = g.at(i, j, k);
         const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
         const double v = div6(sum6(__ldg(cur + c - sx), __ldg(cur + c + sx), __ldg(cur + c - sy),
                                    __ldg(cur + c + sy), __ldg(cur + c - 1), __ldg(cur + c + 1)));
         nxt[c] = v;
-        if (res) worst = fabs(__dsub_rn(v, __ldg(cur + c)));
+        if (res) worst = abs_diff_bits(v, __ldg(cur + c));
     }
     if (res) warp_max_to_global(worst, res);
 }
@@ -468,7 +479,7 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
     __syncthreads();
     const hx::Geom g(by, bz);
     const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
-    double worst = 0.0;
+    unsigned long long worst = 0;
     // One row per CTA iteration: the (box, i, j) decode happens once per row
     // and the threads stream along it (k-contiguous rows coalesce).
     for (int row = blockIdx.x; ok && row < J.rows[J.nbox]; row += gridDim.x) {
@@ -508,7 +519,7 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
             // acquire above (observed through the barrier) orders the loads.
             const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy],
                                        cur[c - 1], cur[c + 1]));
-            if (res) worst = fmax(worst, fabs(__dsub_rn(v, cur[c])));
+            if (res) worst = max(worst, abs_diff_bits(v, cur[c]));
             return v;
         };
         auto put = [&](int t, double v, unsigned skip) {
@@ -819,7 +830,7 @@ stencil_slab_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
                     unsigned long long *res) {
     const hx::Geom g(by, bz);
     const long long n = (long long)ni * nj * nk;
-    double worst = 0.0;
+    unsigned long long worst = 0;
     for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < n;
          q += (long long)gridDim.x * blockDim.x) {
         int i, j, k;
@@ -839,7 +850,7 @@ stencil_slab_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
         const double v = div6(sum6(__ldg(cur + c - sx), __ldg(cur + c + sx), __ldg(cur + c - sy),
                                    __ldg(cur + c + sy), __ldg(cur + c - 1), __ldg(cur + c + 1)));
         nxt[c] = v;
-        if (res) worst = fmax(worst, fabs(__dsub_rn(v, __ldg(cur + c))));
+        if (res) worst = max(worst, abs_diff_bits(v, __ldg(cur + c)));
     }
     if (res) warp_max_to_global(worst, res);
 }
@@ -859,7 +870,7 @@ stencil_zcol_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
     const int lane = threadIdx.x & 31;
     const int j = j0 + blockIdx.x * blockDim.x + threadIdx.x;
     const int i = i0 + blockIdx.y;
-    double worst = 0.0;
+    unsigned long long worst = 0;
     const bool live = j < j1;
     const int jj = live ? j : j1 - 1;  // keep every lane active for the shuffles
     const double2 *row = reinterpret_cast<const double2 *>(cur + g.at(i, jj, ka));
@@ -875,7 +886,7 @@ stencil_zcol_kernel(const double *__restrict__ cur, double *__restrict__ nxt, in
     const double v = div6(sum6(__ldg(cur + at - sx), __ldg(cur + at + sx), ym, yp, zm, zp));
     if (live) {
         nxt[at] = v;
-        if (res) worst = fabs(__dsub_rn(v, ctr));
+        if (res) worst = abs_diff_bits(v, ctr);
     }
     if (res) warp_max_to_global(worst, res);
 }

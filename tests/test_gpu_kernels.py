@@ -367,3 +367,24 @@ def test_row_pipeline_odd_z_sub_boxes(hx):
     want = nxt0.copy()
     jacobi_np.stencil(cur, want)
     assert n.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("variant", [0, 2, 5])
+def test_residual_propagates_nan_like_numpy(hx, variant):
+    """max|nxt - cur| with a NaN in the field is NaN, as numpy's max makes it
+    in the reference (cl/jacobi3d.py:197-198); the C oracle agrees. Without
+    one, the residual is unchanged by the integer-pipe max."""
+    rng = np.random.default_rng(7)
+    shape = (12, 20, 35) if variant == 5 else (12, 20, 34)
+    cur = rng.standard_normal(tuple(s + 2 for s in shape))
+    _, _, clean = run_stencil(hx, cur, variant, res=True)
+    want = cur.copy()
+    assert clean == jacobi_c.stencil_residual(cur, want, nthreads=2) == jacobi_np.residual(cur, want)
+    cur[5, 7, 9] = np.nan
+    nxt0, got, res = run_stencil(hx, cur, variant, res=True)
+    want = nxt0.copy()
+    assert np.isnan(res)
+    assert np.isnan(jacobi_c.stencil_residual(cur, want, nthreads=2))
+    assert np.isnan(jacobi_np.residual(cur, want))
+    # NaN payloads may differ between the GPU's and the host's arithmetic
+    assert np.array_equal(got, want, equal_nan=True)
