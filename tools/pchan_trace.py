@@ -39,9 +39,13 @@ def main():
     ap.add_argument("--sizes", default="1048576")
     ap.add_argument("--window", type=int, default=64)
     ap.add_argument("--slot", type=int, default=0, help="0: as large as the message")
+    ap.add_argument("--pingpong", action="store_true", help="latency timeline instead")
     a = ap.parse_args()
     for size in [int(x) for x in a.sizes.split(",")]:
-        run(a, size)
+        if a.pingpong:
+            pingpong_timeline(size)
+        else:
+            run(a, size)
 
 
 def run(a, size):
@@ -85,6 +89,46 @@ def run(a, size):
           f"{np.median((rh - sp) / 1e3):.2f} us")
     _lib.call("hx_chan_trace", 0, None, None)
     _lib.call("hx_chan_trace", 1, None, None)
+
+
+
+def pingpong_timeline(size: int = 8, iters: int = 64):
+    """Ping-pong (as osu.channel_latency) with stamps: for a few round
+    trips, each GPU's channel events in time order, microseconds from that
+    GPU's first event of the round trip (clocks are per GPU)."""
+    ch = PersistentChannel(0, 1, slot_bytes=64 << 10, depth=2)
+    src = torch.randint(0, 255, (max(size, 1),), dtype=torch.uint8, device="cuda:0")
+    back = torch.zeros(max(size, 1), dtype=torch.uint8, device="cuda:0")
+    mid = torch.zeros(max(size, 1), dtype=torch.uint8, device="cuda:1")
+    t = traces()
+
+    def leader(s):
+        for _ in range(iters):
+            ch.send(0, src, size, stream=s)
+            ch.recv(0, back, size, stream=s)
+
+    def echo(s):
+        for _ in range(iters):
+            ch.recv(1, mid, size, stream=s)
+            ch.send(1, mid, size, stream=s)
+
+    graphs, streams = _graph_pair((0, 1), leader, echo)
+    _replay_pair((0, 1), graphs, streams, 1)
+    ms = _replay_pair((0, 1), graphs, streams, 1)
+    ch.check()
+    print(f"ping-pong {size} B: {ms * 1e3 / iters / 2:.2f} us one-way")
+    s0, r0 = (x.cpu().numpy()[:2048].reshape(256, 8) for x in t[0])
+    s1, r1 = (x.cpu().numpy()[:2048].reshape(256, 8) for x in t[1])
+    names_s = ["entry", "claimed", "published", "pulled", "done"]
+    names_r = ["entry", "pred done", "header seen", "copied"]
+    for k in range(2 * iters - 4, 2 * iters - 1):  # direction 0 message k, direction 1 message k
+        kk = k & 255
+        for gpu, (snd, rcv, who) in enumerate(((s0, r0, "leader"), (s1, r1, "echo"))):
+            ev = [(snd[kk][i], f"send {names_s[i]}") for i in range(5) if snd[kk][i]]
+            ev += [(rcv[kk][i], f"recv {names_r[i]}") for i in range(4) if rcv[kk][i]]
+            ev.sort()
+            base = ev[0][0]
+            print(f"  k={k} {who}: " + ", ".join(f"{n} {(v - base) / 1e3:.2f}" for v, n in ev))
 
 
 if __name__ == "__main__":
