@@ -384,7 +384,11 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
     __shared__ int ok;
     __shared__ unsigned long long k;
     const unsigned long long t_in = c.trace ? hx::globaltimer() : 0;
-    if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
+    // The claim and the slot wait touch only this direction's channel state,
+    // so even a send that must wait for its predecessor does them first,
+    // overlapped with that predecessor: it was launched after its
+    // predecessor triggered, which (a receive) happens after that one's own
+    // wait, so every earlier send of the stream has completed its claim.
     if (threadIdx.x == 0) {
         k = chan_claim(c.seq);
         if (blockIdx.x == 0 && c.trace) c.trace[(k & 255) * 8] = t_in;
@@ -397,6 +401,10 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
     }
     __syncthreads();
     if (blockIdx.x == 0 && threadIdx.x == 0) chan_stamp(c, k, 1);
+    // Not early: the predecessor may be writing the source. Wait for it
+    // before reading the source — and before triggering, so a following
+    // early send of the same buffer cannot start ahead of that writer.
+    if (!early) asm volatile("griddepcontrol.wait;" ::: "memory");
     // only now may the next send launch: a launch never waits on a later one
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     char *slot = c.slots + (k % c.depth) * c.stride;
