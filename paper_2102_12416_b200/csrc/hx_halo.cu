@@ -324,13 +324,11 @@ __device__ __forceinline__ bool chan_last_cta(unsigned int *counter, int sys_fen
 
 // Programmatic dependent launch: channel kernels are launched with
 // programmatic stream serialisation, so the next operation on the stream is
-// scheduled while this one runs; each still waits for its predecessor's
-// completion (and memory) before it touches the channel state. The device
-// counters keep the exact stream order; only the launch latency overlaps.
-__device__ __forceinline__ void chan_dependent_prologue() {
-    asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
+// scheduled while this one runs. Each kernel claims its message index (a
+// ticket word), reads what it may read early, and waits for its predecessor
+// (griddepcontrol.wait) before any write its predecessor could conflict
+// with; the device tickets keep the exact stream order, and only launch
+// latency and reads overlap.
 
 __device__ __forceinline__ unsigned load4(const unsigned char *p, unsigned long long avail) {
     if (avail >= 4 && ((uintptr_t)p & 3) == 0) return *reinterpret_cast<const unsigned *>(p);
@@ -461,13 +459,26 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
     __shared__ unsigned long long k, len;
     __shared__ const char *from;
     const unsigned long long t_in = c.trace ? hx::globaltimer() : 0;
-    chan_dependent_prologue();
+    // Everything up to the predecessor wait only READS: the message index
+    // (claimed like a send's: receives on a stream claim in launch order,
+    // each launched after its predecessor passed its own wait), the header,
+    // and the first round of the payload into registers. So a receive
+    // launched behind another one finds its message and loads it while that
+    // one still copies, and only its stores wait. (It runs behind a send
+    // only once that send has passed its own wait and claim.)
     if (threadIdx.x == 0) {
-        k = *(volatile unsigned long long *)c.seq;
-        if (blockIdx.x == 0 && c.trace) {
-            c.trace[(k & 255) * 8] = t_in;
-            chan_stamp(c, k, 1);
-        }
+        k = chan_claim(c.seq);
+        if (blockIdx.x == 0 && c.trace) c.trace[(k & 255) * 8] = t_in;
+    }
+    // When may the next operation launch? A one-CTA receive lets it launch
+    // at once: a send behind it (the echo of a ping-pong) then claims and
+    // waits for its slot while this receive still polls, so the send's launch
+    // latency is off the critical path. A multi-CTA receive triggers only
+    // once its message has arrived, which bounds the receives in flight (each
+    // up to 2 x SMs CTAs) to the messages already delivered.
+    __syncthreads();
+    if (gridDim.x == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    if (threadIdx.x == 0) {
         const unsigned long long tag = (k + 1) & 0xffffffffull;
         const unsigned long long *hdr =
             reinterpret_cast<const unsigned long long *>(c.slots + (k % c.depth) * c.stride);
@@ -491,17 +502,32 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
         }
     }
     __syncthreads();
+    if (gridDim.x > 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     const char *slot = c.slots + (k % c.depth) * c.stride;
     const unsigned long long take = len < capacity ? len : capacity;
     const unsigned long long tag = (k + 1) & 0xffffffffull;
-    if (ok && pull) {  // straight out of the sender's buffer (peer loads, L2 only)
-        copy_bytes((char *)dst, from, take, blockIdx.x * (size_t)blockDim.x + threadIdx.x,
-                   (size_t)gridDim.x * blockDim.x, true);
-    } else if (ok && len <= HX_CHAN_LL_MAX) {
+    const size_t tid = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+    const size_t nth = (size_t)gridDim.x * blockDim.x;
+    const bool ll = ok && len <= HX_CHAN_LL_MAX;
+    const char *from_p = pull ? from : slot + CHAN_HDR;  // pull: the sender's buffer over NVLink
+    const bool vec = ok && !ll && ((((uintptr_t)dst | (uintptr_t)from_p) & 15) == 0);
+    const size_t nv = vec ? take / 16 : 0;
+    constexpr int R = 4;    // bulk: 16-byte vectors per thread in the first round
+    constexpr int LLW = 8;  // LL: words per thread (HX_CHAN_LL_MAX / 4 / 256)
+    uint4 pre[R];
+    unsigned words_v[LLW];
+    if (vec) {
+        const uint4 *s16 = reinterpret_cast<const uint4 *>(from_p);
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+            if (tid + u * nth < nv) pre[u] = __ldcg(s16 + tid + u * nth);
+    } else if (ll) {
         const unsigned long long *words = reinterpret_cast<const unsigned long long *>(slot + CHAN_HDR);
         const unsigned long long n = (take + 3) / 4;
-        for (unsigned long long w = blockIdx.x * (size_t)blockDim.x + threadIdx.x; w < n;
-             w += (size_t)gridDim.x * blockDim.x) {
+#pragma unroll
+        for (int u = 0; u < LLW; ++u) {
+            const size_t w = tid + u * nth;
+            if (w >= n) break;
             unsigned long long v;
             unsigned polls = 0;
             const unsigned long long t0 = hx::globaltimer();
@@ -511,12 +537,30 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
                     break;
                 }
             }
-            store4(dst + 4 * w, (unsigned)v, take - 4 * w);
+            words_v[u] = (unsigned)v;
         }
-    } else if (ok) {
-        copy_bytes((char *)dst, slot + CHAN_HDR, take,
-                   blockIdx.x * (size_t)blockDim.x + threadIdx.x, (size_t)gridDim.x * blockDim.x,
-                   true);
+    }
+    // the predecessor may still read or write dst: stores only from here on
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (blockIdx.x == 0 && threadIdx.x == 0) chan_stamp(c, k, 1);
+    if (vec) {
+        uint4 *d16 = reinterpret_cast<uint4 *>(dst);
+#pragma unroll
+        for (int u = 0; u < R; ++u)
+            if (tid + u * nth < nv) d16[tid + u * nth] = pre[u];
+        const uint4 *s16 = reinterpret_cast<const uint4 *>(from_p);
+        for (size_t q = tid + R * nth; q < nv; q += nth) d16[q] = __ldcg(s16 + q);
+        for (size_t b = nv * 16 + tid; b < take; b += nth) dst[b] = from_p[b];
+    } else if (ll) {
+        const unsigned long long n = (take + 3) / 4;
+#pragma unroll
+        for (int u = 0; u < LLW; ++u) {
+            const size_t w = tid + u * nth;
+            if (w >= n) break;
+            store4(dst + 4 * w, words_v[u], take - 4 * w);
+        }
+    } else if (ok) {  // unaligned bulk or pull
+        copy_bytes((char *)dst, from_p, take, tid, nth, true);
     }
     // no fence before the arrival count: a CTA's slot (or source) reads are
     // complete once the barrier passed — their values fed stores issued
@@ -527,7 +571,6 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
         // every thread's slot reads fed its stores before the barrier, so
         // the slot may be handed back without a fence
         st_relaxed_sys(c.credit, k + 1);
-        *c.seq = k + 1;
     }
 }
 

@@ -68,6 +68,7 @@ class PersistentChannel:
             rdev, tdev = torch.device("cuda", rx), torch.device("cuda", tx)
             self._dir.append({
                 "slots": torch.zeros(depth * self.stride, dtype=torch.uint8, device=rdev),
+                # receive ticket (message index << 32 | CTAs of the current launch)
                 "rseq": torch.zeros(1, dtype=torch.int64, device=rdev),
                 # credit, ticket (message index << 32 | CTAs of the current launch)
                 "tmeta": torch.zeros(2, dtype=torch.int64, device=tdev),
@@ -141,7 +142,7 @@ class PersistentChannel:
         """Per direction: (sent, received) message counts (device state)."""
         out = []
         for d in self._dir:
-            out.append((int(d["tmeta"][1].item()) >> 32, int(d["rseq"][0].item())))
+            out.append((int(d["tmeta"][1].item()) >> 32, int(d["rseq"][0].item()) >> 32))
         return out
 
     def close(self) -> None:
