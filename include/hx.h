@@ -199,11 +199,14 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
  * address and the receive copies straight out of the sender's buffer over
  * NVLink (one copy, any size below 2^31 bytes), the send completing when
  * the slot comes back. The message index is device state (*seq, one per endpoint,
- * advanced by each launch; for the sender a ticket word: index << 32 | CTAs
- * of the launch arrived), so send/recv sequences can be captured in CUDA
- * graphs. Consecutive sends on one stream overlap on the GPU (each claims
- * its index and slot, then lets the next launch start) and still complete
- * in stream order; a send after a receive on the same stream waits for it.
+ * advanced by each launch; a ticket word: index << 32 | CTAs of the launch
+ * arrived), so send/recv sequences can be captured in CUDA graphs.
+ * Consecutive sends on one stream overlap on the GPU (each claims its index
+ * and slot, then lets the next launch start) and still complete in stream
+ * order; a send after a receive on the same stream claims early but reads
+ * its source only after that receive completed. A receive claims, polls its
+ * header and loads the first round of its payload before waiting for its
+ * predecessor; only its stores wait.
  *   send k: wait until *credit >= k+1-depth (slot k % depth free), write
  *           the payload into the slot (a peer-mapped pointer) and its header.
  *   recv k: wait for the header tag, copy min(len, capacity) bytes into dst,
