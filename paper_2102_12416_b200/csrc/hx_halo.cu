@@ -371,8 +371,9 @@ __device__ __forceinline__ unsigned long long chan_claim(unsigned long long *tic
 // kernel triggers at its completion). Send k+1 claims its index and slot,
 // copies and publishes while send k still runs; it waits for its
 // predecessor only at its end, so sends still complete in stream order.
-// Without `early` the send waits for its predecessor first (a preceding
-// receive may be writing the buffer this send reads).
+// Without `early` the send waits for its predecessor before it reads the
+// source or lets the next launch start (a preceding receive may be writing
+// the buffer this send reads).
 // flags: bit 0 early; bits 1-2 per-CTA fence mode of a bulk send
 // (chan_last_cta); bits 8-15 the launch serial (diagnostics, hx_chan_trace).
 __global__ void __launch_bounds__(1024)
@@ -384,9 +385,9 @@ chan_send_kernel(ChanDir c, const unsigned char *src, unsigned long long bytes,
     const unsigned long long t_in = c.trace ? hx::globaltimer() : 0;
     // The claim and the slot wait touch only this direction's channel state,
     // so even a send that must wait for its predecessor does them first,
-    // overlapped with that predecessor: it was launched after its
-    // predecessor triggered, which (a receive) happens after that one's own
-    // wait, so every earlier send of the stream has completed its claim.
+    // overlapped with that predecessor. Claims stay in stream order: every
+    // channel kernel claims before it triggers its dependents, and a launch
+    // starts only after its predecessor triggered.
     if (threadIdx.x == 0) {
         k = chan_claim(c.seq);
         if (blockIdx.x == 0 && c.trace) c.trace[(k & 255) * 8] = t_in;
@@ -460,12 +461,10 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
     __shared__ const char *from;
     const unsigned long long t_in = c.trace ? hx::globaltimer() : 0;
     // Everything up to the predecessor wait only READS: the message index
-    // (claimed like a send's: receives on a stream claim in launch order,
-    // each launched after its predecessor passed its own wait), the header,
-    // and the first round of the payload into registers. So a receive
-    // launched behind another one finds its message and loads it while that
-    // one still copies, and only its stores wait. (It runs behind a send
-    // only once that send has passed its own wait and claim.)
+    // (claimed like a send's, so receives claim in stream order), the
+    // header, and the first round of the payload into registers. So a
+    // receive launched behind another one finds its message and loads it
+    // while that one still copies, and only its stores wait.
     if (threadIdx.x == 0) {
         k = chan_claim(c.seq);
         if (blockIdx.x == 0 && c.trace) c.trace[(k & 255) * 8] = t_in;
