@@ -388,7 +388,8 @@ def p2p_probe() -> dict | None:
     """OSU-style point to point between GPUs 0 and 1 (configs[1]): 8-byte
     one-way latency and 4 MiB window bandwidth, device level (one kernel
     per side: LL ping-pong; pull window) and through the pre-registered
-    persistent channel (graph-replayed send/recv). None on a 1-GPU box."""
+    persistent channel (graph-replayed send/recv; 64 KiB slots, so the
+    4 MiB messages are pulled by the receive). None on a 1-GPU box."""
     import torch
 
     if torch.cuda.device_count() < 2:

@@ -30,7 +30,11 @@ def main():
         ("mpi dev lat", lambda s: lat(pick(s, benchmark="latency", api="mpi", mode="device"))),
         ("chan host-staged lat", lambda s: lat(pick(s, benchmark="latency", api="charm-channel", mode="host"))),
         ("persistent chan lat (µs)", lambda s: lat(pick(s, benchmark="channel-latency"))),
-        ("persistent chan bw (GB/s)", lambda s: bw(pick(s, benchmark="channel-bandwidth"))),
+        ("persistent chan bw (GB/s)", lambda s: bw(pick(s, benchmark="channel-bandwidth",
+                                                        slot_bytes=65536))),
+        ("persistent chan bw, message-sized slots", lambda s: bw(
+            pick(s, benchmark="channel-bandwidth", protocol="slot", slot_bytes=max(s, 16)))
+            if s > 65536 else "="),
         ("chan dev bw (GB/s)", lambda s: bw(pick(s, benchmark="bandwidth", api="charm-channel", mode="device"))),
         ("msg dev bw", lambda s: bw(pick(s, benchmark="bandwidth", api="charm-messaging", mode="device"))),
         ("device lat (µs)", lambda s: lat(pick(s, benchmark="device-latency"))),

@@ -57,7 +57,9 @@ def main():
             emit({**r, "level": "api", "gpus": min(ngpu, 2)})
         if ngpu >= 2:
             emit(channel_latency(size, iters=1000 if size <= 65536 else 200, warmup=20))
-            emit(channel_bandwidth(size, window=64, iters=5))
+            emit(channel_bandwidth(size, window=64, iters=5))  # 64 KiB slots: pull above
+            if size > (64 << 10):  # slots as large as the message: push into the slot
+                emit(channel_bandwidth(size, window=64, iters=5, slot_bytes=None))
             emit({**device_latency(size, iters=2000 if size <= 65536 else 200, warmup=50),
                   "level": "device"})
             for engine in ("ce", "sm", "sm-pull", "sm-window", "sm-pull-window"):
