@@ -226,6 +226,14 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
                  unsigned long long *credit, unsigned long long *seq, unsigned int *counter,
                  unsigned long long *len_out, unsigned long long timeout_ns, int *err,
                  void *stream);
+/* Load every spinning channel / exchange kernel on the current device now.
+ * Under lazy module loading (PyTorch's default) a kernel's first launch can
+ * stall behind kernels spinning on the device until their waits time out;
+ * PersistentChannel and HaloJacobi call this for each device they use.
+ * Kernels a caller interleaves with channel operations should likewise run
+ * once beforehand (or set CUDA_MODULE_LOADING=EAGER). */
+int hx_preload(void);
+
 /* Diagnostics: channel operations launched on `device` afterwards write
  * %globaltimer stamps — 8 per message, message k at [(k % 256) * 8] — into
  * send_trace / recv_trace (device buffers of 2048 uint64 — send: 2048 +

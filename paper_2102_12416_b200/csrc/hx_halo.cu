@@ -889,6 +889,24 @@ static cudaLaunchConfig_t chan_launch_config(unsigned grid, void *stream, cudaLa
     return cfg;
 }
 
+// Lazy module loading (CUDA_MODULE_LOADING=LAZY, PyTorch's default) loads a
+// kernel at its first launch, and that load can stall behind kernels that
+// are spinning on the device, e.g. a receive waiting for a message that the
+// newly loaded kernel's stream must produce: the spin then only ends at its
+// timeout. Channel and exchange users preload every spinning or
+// interleaved kernel of this file on each device they use.
+int hx_preload_halo_kernels() {
+    cudaFuncAttributes a;
+    const void *k[] = {(const void *)chan_send_kernel, (const void *)chan_recv_kernel,
+                       (const void *)copy_kernel, (const void *)copy_window_kernel,
+                       (const void *)pack_put_kernel, (const void *)wait_unpack_kernel,
+                       (const void *)face_copy_kernel<true>, (const void *)face_copy_kernel<false>,
+                       (const void *)signal_kernel, (const void *)wait_flag_kernel,
+                       (const void *)pingpong_kernel, (const void *)pingpong_ll_kernel};
+    for (const void *f : k) HX_TRY(cudaFuncGetAttributes(&a, f));
+    return 0;
+}
+
 // The last channel operation enqueued on each stream (true = a send): a send
 // right after a send may overlap it (chan_send_kernel `early`).
 static std::mutex chan_last_mu;

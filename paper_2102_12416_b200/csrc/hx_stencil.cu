@@ -987,6 +987,18 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
     return launch_generic(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);
 }
 
+int hx_preload_halo_kernels();  // hx_halo.cu
+
+// See hx_preload_halo_kernels: the exchange's spinning kernels, loaded up
+// front on the current device (the stencil variants are launched alone or
+// concurrently with the fused shell, which needs no other kernel to finish).
+int hx_preload() {
+    cudaFuncAttributes a;
+    HX_TRY(cudaFuncGetAttributes(&a, (const void *)shell_put_kernel));
+    HX_TRY(cudaFuncGetAttributes(&a, (const void *)fill_kernel));
+    return hx_preload_halo_kernels();
+}
+
 int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbox,
                  const int *boxes, double *const remote[6], unsigned long long *const wait_flag[6],
                  unsigned long long wait_value, unsigned long long *const signal_flag[6],

@@ -230,6 +230,9 @@ class HaloJacobi:
 
     def reset(self) -> None:
         """Dirichlet initial state (cl/jacobi3d.py:131-138) and zeroed flags."""
+        for dev in sorted({b.device for b in self.blocks.values()}):
+            _lib.call("hx_set_device", dev)
+            _lib.call("hx_preload")  # no lazy kernel load behind a spinning one (include/hx.h)
         for b in self.blocks.values():
             s = self.stream_of(b).cuda_stream
             _lib.call("hx_set_device", b.device)

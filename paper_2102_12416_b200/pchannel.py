@@ -59,6 +59,9 @@ class PersistentChannel:
         self.timeout_ns = int(timeout_s * 1e9)
         _lib.call("hx_enable_peer", gpu_a, gpu_b)
         _lib.call("hx_enable_peer", gpu_b, gpu_a)
+        for g in (gpu_a, gpu_b):  # no lazy kernel load behind a spinning one
+            _lib.call("hx_set_device", g)
+            _lib.call("hx_preload")
         # a slot: header block, then the payload (LL words are 2x the bytes)
         ll = min(slot_bytes, LL_MAX)
         self.stride = -(-(HDR + max(slot_bytes, 8 * (-(-ll // 4)))) // 256) * 256

@@ -306,3 +306,71 @@ def test_persistent_channel_overlapping_claims_are_ordered(cuda):
             seen += 1
             assert v.min() == v.max(), f"one launch claimed indices {sorted(set(v - 1))}"
     assert seen >= window
+
+
+@needs2
+@pytest.mark.parametrize("seed", range(4))
+def test_persistent_channel_random_schedules(cuda, seed):
+    """Randomised traffic in both directions at once, each endpoint with a
+    send stream and a receive stream (so no schedule can deadlock): random
+    message sizes across the LL / slot / pull protocols, random receive
+    capacities (truncation), bursts of back-to-back sends (overlapping
+    launches) interleaved with ordinary kernels that rewrite a shared
+    source, and depth-1 and depth-3 rings. Every receive must report the
+    k-th message of its direction, truncated to its capacity, exactly."""
+    from paper_2102_12416_b200.completion import OK, TRUNCATED
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    rng = np.random.default_rng(1000 + seed)
+    slot = 40000
+    ch = PersistentChannel(0, 1, slot_bytes=slot, depth=1 + 2 * (seed % 2), timeout_s=20)
+    send_s = [torch.cuda.Stream(device=e) for e in (0, 1)]
+    recv_s = [torch.cuda.Stream(device=e) for e in (0, 1)]
+    choices = [1, 8, 1000, 8192, 8193, 30000, slot, slot + 1, 200000, 1 << 20]
+    n = 30
+    sizes = [[int(rng.choice(choices)) for _ in range(n)] for _ in (0, 1)]
+    caps = [[int(rng.choice([s, s, s, max(1, s // 3), s + 7])) for s in sizes[e]] for e in (0, 1)]
+    shared = [torch.zeros(1 << 20, dtype=torch.uint8, device=f"cuda:{e}") for e in (0, 1)]
+    # Sources are uploaded before any send is enqueued: a pulled send holds
+    # its stream until the matching receive exists, and a pageable upload
+    # on that stream would block the host before it enqueues the receives.
+    plan = [[], []]
+    for e in (0, 1):
+        for size in sizes[e]:
+            if rng.random() < 0.3:  # an ordinary kernel rewrites the shared source first
+                plan[e].append((int(rng.integers(0, 256)), None))
+            else:
+                m = rng.integers(0, 256, size, dtype=np.uint8)
+                plan[e].append((None, (m, torch.from_numpy(m).to(f"cuda:{e}"))))
+    for e in (0, 1):  # load torch's fill kernel now: a lazily loaded kernel can stall
+        shared[e].fill_(1)  # behind spinning channel kernels (include/hx.h, hx_preload)
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    want = [[], []]
+    for e in (0, 1):  # endpoint e sends on direction e
+        for k, size in enumerate(sizes[e]):
+            v, own = plan[e][k]
+            if own is None:
+                with torch.cuda.stream(send_s[e]):
+                    shared[e].fill_(v)
+                src = shared[e]
+                want[e].append(np.full(size, v, dtype=np.uint8))
+            else:
+                want[e].append(own[0])
+                src = own[1]
+            ch.send(e, src, size, stream=send_s[e])
+    sinks, tickets = [[], []], [[], []]
+    for e in (0, 1):  # endpoint 1 - e receives direction e
+        for k in range(n):
+            sink = torch.zeros(max(caps[e][k], 1), dtype=torch.uint8, device=f"cuda:{1 - e}")
+            sinks[e].append(sink)
+            tickets[e].append(ch.recv(1 - e, sink, caps[e][k], stream=recv_s[1 - e]))
+    ch.check()
+    for e in (0, 1):
+        for k in range(n):
+            size, cap = sizes[e][k], caps[e][k]
+            st, length = ch.completion(1 - e, tickets[e][k], cap)
+            assert length == size and st == (OK if cap >= size else TRUNCATED), (e, k)
+            take = min(size, cap)
+            assert np.array_equal(sinks[e][k][:take].cpu().numpy(), want[e][k][:take]), (e, k)
+    assert ch.counters == [(n, n), (n, n)]
