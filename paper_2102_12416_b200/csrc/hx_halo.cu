@@ -836,7 +836,7 @@ int hx_move(void *dst, const void *src, size_t bytes, int device, void *stream, 
 // diagnostics; tools/pchan_knobs.py sweeps them one process per setting).
 // Sends overlap each other, so each needs few CTAs: HX_CHAN_SEND_CTAS
 // (default 64) x HX_CHAN_SEND_THREADS (256 / 512 / 1024, default 512);
-// receives HX_CHAN_RECV_CTAS (default 3 x SMs) x 256. HX_CHAN_DIAG_FENCE:
+// receives HX_CHAN_RECV_CTAS (default 2 x SMs) x 256. HX_CHAN_DIAG_FENCE:
 // the per-CTA fence of a bulk send (chan_last_cta): 0 GPU scope (default),
 // 1 system scope, 2 none (diagnostics only). profiles/r1_pchannel.md.
 struct ChanKnobs {
@@ -970,9 +970,13 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
     chan_note(stream, false);
     cudaLaunchAttribute attr;
     // sized by the sink: a pulled message may be far larger than a slot
-    // 3 x SMs (all fit at 80 registers x 256 threads): a pulled 4 MiB message
-    // is then loaded entirely before the predecessor wait (4 x 16 B a thread)
-    const unsigned cap = chan_knobs().recv_ctas ? chan_knobs().recv_ctas : 3 * chan_sms();
+    // 2 x SMs: a pulled 4 MiB message is loaded entirely before the
+    // predecessor wait (4 x 16 B a thread), and a receive spinning on its
+    // header holds at most ~60 % of the register file (80 x 256 per CTA), so
+    // a 64-CTA bulk send can still run beside it. 3 x SMs (94 %) was 10 %
+    // faster for pulled 16 MiB windows but could starve the send that the
+    // peer's message depends on.
+    const unsigned cap = chan_knobs().recv_ctas ? chan_knobs().recv_ctas : 2 * chan_sms();
     const unsigned grid = chan_grid(capacity, cap, 16384);
     const cudaLaunchConfig_t cfg = chan_launch_config(grid, stream, &attr);
     HX_TRY(cudaLaunchKernelEx(&cfg, chan_recv_kernel, c, (unsigned char *)dst,
