@@ -57,13 +57,21 @@ def hbm_peak():
         return 6650.0, "fallback"
 
 
-def ncu_traffic():
-    """dram bytes per stencil launch from the committed ncu --set full summary."""
+def ncu_traffic(alg_bytes):
+    """(dram bytes per stencil launch, capture's traffic / algorithmic ratio)
+    from the committed ncu --set full summary. The bytes are reported only
+    when the capture is of a launch of this size (same algorithmic bytes);
+    a capture of another block size is not this launch's traffic."""
     try:
         with open(os.path.join(ROOT, "profiles", "stencil_ncu_summary.json")) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
     except Exception:
-        return None
+        return None, None
+    cap_alg = d.get("alg_bytes_per_launch")
+    ratio = d.get("traffic_over_alg")
+    if cap_alg and abs(cap_alg - alg_bytes) <= 0.001 * cap_alg:
+        return d.get("dram_bytes_per_launch"), ratio
+    return None, ratio
 
 
 class ClockSampler:
@@ -311,6 +319,7 @@ def main() -> int:
     value = total_cells * args.steps / (t_ms * 1e-3) / 1e9
     peak, peak_kind = hbm_peak()
     achieved = ALG_BYTES_PER_CELL * sweep_cells / (sten_ms * 1e-3) / 1e9
+    traffic, traffic_ratio = ncu_traffic(ALG_BYTES_PER_CELL * sweep_cells)
     face_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs)
 
     # ---- the exchange alone (not sharing HBM with an interior sweep): a few
@@ -353,7 +362,8 @@ def main() -> int:
                        "l2": f"inputs > L2 (2 x {(b.bx + 2) * (b.by + 2) * (b.bz + 2) * 8 / 1e9:.1f} GB "
                              "fields per GPU vs 126 MB L2), no flush needed"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(),
+                         "frac": achieved / peak, "traffic": traffic,
+                         "traffic_over_alg_1536_capture": traffic_ratio,
                          "kernel": "stencil_tma_kernel", "peak_kind": peak_kind,
                          "kernel_ms": sten_ms,
                          "alg_bytes_per_launch": ALG_BYTES_PER_CELL * sweep_cells},
