@@ -67,10 +67,11 @@ def ncu_traffic(alg_bytes):
             d = json.load(f)
     except Exception:
         return None, None
-    cap_alg = d.get("alg_bytes_per_launch")
     ratio = d.get("traffic_over_alg")
-    if cap_alg and abs(cap_alg - alg_bytes) <= 0.001 * cap_alg:
-        return d.get("dram_bytes_per_launch"), ratio
+    for cap in [d] + d.get("other_captures", []):
+        cap_alg = cap.get("alg_bytes_per_launch")
+        if cap_alg and abs(cap_alg - alg_bytes) <= 0.001 * cap_alg:
+            return cap.get("dram_bytes_per_launch"), ratio
     return None, ratio
 
 
