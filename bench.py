@@ -17,9 +17,17 @@ bounded slab sample), e2e through the public API with host buffers
 (per-step H2D of the Dirichlet hot-wall plane from pinned memory, per-step
 D2H of the residual), clocks sampled during the timed region.
 
---impl reference: the reference's own CPU algorithm (its C restatement in
-oracle/, bit-identical to the numpy reference) on all host cores, same
-metric/config, each step a bounded slab sample of the per-GPU block.
+Also on the line: data_alt (the same timed steps on a seeded N(0,1)
+interior: speed must not come from the hot wall's zeros) and, at N=1,
+e2e_api (the reference's entry point run_jacobi(mode="channel-persistent")
+end to end, field read-back included).
+
+--impl reference: the reference's OWN code (charmlet, installed unmodified
+into baseline/_ref): _BlockCore.update (numpy, cl/jacobi3d.py:165-173) in
+one pinned process per host core, each on a 16-plane slab block of the
+per-GPU cross-section; plus its run_jacobi 64^3 x 100 and OSU 8 B / 4 MiB
+numbers in wall mode (reference_api). Falls back to the bit-identical C
+restatement in oracle/ when baseline/_ref is absent.
 """
 
 from __future__ import annotations
@@ -168,26 +176,130 @@ def cpu_sample(block: int, seconds: float):
 
 # ------------------------------------------------------------- reference arm
 
+REF_DIR = os.path.join(ROOT, "baseline", "_ref")
+
+
+def reference_available() -> bool:
+    return os.path.isdir(os.path.join(REF_DIR, "charmlet"))
+
+
+def _ref_update_worker(core_id, planes, block, steps, conn):
+    """One host core: the reference's own _BlockCore.update (numpy,
+    cl/jacobi3d.py:165-173) on a (planes, block, block) slab block, one
+    update per step when the parent says go."""
+    try:
+        os.sched_setaffinity(0, {core_id})
+    except Exception:
+        pass
+    sys.path.insert(0, REF_DIR)
+    from charmlet.devicesim import DeviceSpace
+    from charmlet.jacobi3d import _BlockCore
+
+    space = DeviceSpace(None, {}, 1 << 42)
+    core = _BlockCore((planes, block, block), (1, 1, 1), 0, lambda n: space.alloc(0, n))
+    core.update()  # first touch of every page + numpy temporaries
+    conn.send("ready")
+    for _ in range(steps):
+        conn.recv()
+        t0 = time.perf_counter()
+        core.update()
+        conn.send(time.perf_counter() - t0)
+    conn.close()
+
+
+def reference_update_sample(block: int, steps: int, warmup: int, planes: int = 16):
+    """Aggregate GLUP/s of the reference's numpy stencil on every host core:
+    one pinned process per core, each sweeping its own slab of the per-GPU
+    block's cross-section; a step = one update in every process, started
+    together, timed to the last one to finish."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("fork")
+    cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(
+        range(os.cpu_count() or 1))
+    procs, pipes = [], []
+    for c in cores:
+        a, b = ctx.Pipe()
+        p = ctx.Process(target=_ref_update_worker, args=(c, planes, block, warmup + steps, b))
+        p.start()
+        procs.append(p)
+        pipes.append(a)
+    for a in pipes:
+        assert a.recv() == "ready"
+    times = []
+    for k in range(warmup + steps):
+        t0 = time.perf_counter()
+        for a in pipes:
+            a.send("go")
+        for a in pipes:
+            a.recv()
+        if k >= warmup:
+            times.append(time.perf_counter() - t0)
+    for p in procs:
+        p.join()
+    cells = len(cores) * planes * block * block
+    t = statistics.median(times)
+    return {"value": cells / t / 1e9, "unit": UNIT, "cores": len(cores), "kind": "reference",
+            "step_s": t,
+            "sample": f"reference charmlet _BlockCore.update (numpy, baseline/_ref) in {len(cores)} "
+                      f"processes pinned one per core, each on its own {planes}x{block}x{block} "
+                      f"slab block; step = one update in every process (median of {steps})"}
+
+
+def reference_api_sample():
+    """The reference's own drivers in wall mode on one core:
+    run_jacobi 64^3 x 100 (channel-device, 1/2/4/8 PEs) and the OSU 8 B
+    latency / 4 MiB window bandwidth of both APIs (cl/jacobi3d.py:335-379,
+    cl/bench.py:364-452)."""
+    sys.path.insert(0, REF_DIR)
+    from charmlet import bench as rbench
+    from charmlet.config import RuntimeConfig
+    from charmlet.jacobi3d import run_jacobi as rjacobi
+
+    out = {"run_jacobi_64x100_ms_per_iter": {}, "osu": {}}
+    for pes in (1, 2, 4, 8):
+        r = rjacobi((64, 64, 64), 100, "channel-device", pes, cfg=RuntimeConfig(time_mode="wall"))
+        out["run_jacobi_64x100_ms_per_iter"][str(pes)] = r["total_ns"] / 100 / 1e6
+    cfg = rbench.bench_config(time_mode="wall")
+    for api in ("charm-channel", "charm-messaging"):
+        lat = rbench.measure_latency(api, "device", 8, cfg=cfg)
+        bw = rbench.measure_bandwidth(api, "device", 4 << 20, cfg=cfg)
+        out["osu"][api] = {"latency_8B_us": lat["value_ns"] / 1e3,
+                           "bandwidth_4MiB_gbs": bw["value_gbps"],
+                           "verified": lat["verified"] and bw["verified"]}
+    out["cores"] = 1
+    return out
+
+
 def run_reference(args, rank: int) -> int:
     if rank != 0:
         return 0
     n = args.gpus
     dims = global_dims(n, args.block)
-    per_step = max(1.0, args.ref_seconds / max(1, args.steps))
-    for _ in range(args.warmup):
-        cpu_sample(args.block, min(per_step, 2.0))
-    vals = [cpu_sample(args.block, per_step) for _ in range(args.steps)]
-    v = statistics.median(x["value"] for x in vals)
+    if reference_available():
+        cpu = reference_update_sample(args.block, args.steps, args.warmup)
+        v = cpu["value"]
+        extra = {"reference_api": reference_api_sample()}
+    else:  # the reference install is missing: its bit-identical C restatement
+        per_step = max(1.0, args.ref_seconds / max(1, args.steps))
+        for _ in range(args.warmup):
+            cpu_sample(args.block, min(per_step, 2.0))
+        vals = [cpu_sample(args.block, per_step) for _ in range(args.steps)]
+        v = statistics.median(x["value"] for x in vals)
+        cpu = dict(vals[0], value=v)
+        extra = {}
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": n,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": args.block ** 3 * n / (v * 1e9) * 1e3,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
-            "config": {"workload": "Jacobi3D 1536^3 per GPU fp64 weak scaling",
+            "config": {"workload": f"Jacobi3D {args.block}^3 per GPU fp64 weak scaling",
                        "global_dims": list(dims), "block": [args.block] * 3},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": vals[0]["cores"], "kind": "port",
-                             "sample": vals[0]["sample"]},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "cpu_baseline": {k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "note": "ms_per_step extrapolates the measured per-cell rate to the whole per-GPU "
+                    "block (1536^3 does not fit the reference's numpy path in host RAM)"}
+    line.update(extra)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -209,6 +321,13 @@ def main() -> int:
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-p2p", action="store_true", help="skip the GPU 0 <-> 1 OSU probe")
+    ap.add_argument("--data", choices=("hotwall", "random"), default="hotwall",
+                    help="hotwall: the reference's Dirichlet input (interior 0, x=0 plane 1.0); "
+                         "random: seeded N(0,1) interior, same walls. The line also carries a "
+                         "data_alt leg timed on the other input (--no-data-alt skips it)")
+    ap.add_argument("--no-data-alt", action="store_true")
+    ap.add_argument("--no-e2e-api", action="store_true",
+                    help="skip the run_jacobi end-to-end leg (N=1 only)")
     ap.add_argument("--policy", choices=("b200", "reference"), default="b200",
                     help="block decomposition: reference = cl/jacobi3d.py:62-76 exactly; b200 = "
                          "same face area, ties broken away from splitting z (strided faces)")
@@ -268,26 +387,17 @@ def main() -> int:
         return float(t.item())
 
     # ---- device-timed steps (inputs resident in HBM)
+    data_desc = {"hotwall": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
+                 "random": "synthetic (seeded N(0,1) interior, Dirichlet hot-wall ghost planes)"}
+    if args.data == "random":
+        barrier()
+        eng.fill_random(seed=1)
+        barrier()
+    live, t_local, clk = timed_steps(eng, b, args.steps, args.warmup, barrier, local)
     timing: dict = {}
-    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        for _ in range(args.warmup):
-            eng.step()
-        barrier()
-        # the dominant kernel (the interior / full sweep) is timed live inside
-        # the timed steps by one CUDA event pair per step on its own stream;
-        # the other breakdown events (shell, exposed wait) come from a
-        # separate pass so the timed steps carry only that pair
-        split = (eng.overlap or eng.exchange == "fused") and bool(b.nbr_dirs)
-        live = {"_only": {"interior" if split else "sweep"}}
-        start.record(s)
-        for _ in range(args.steps):
-            eng.step(timing=live)
-        stop.record(s)
-        barrier()
-        for _ in range(min(args.steps, 10)):
-            eng.step(timing=timing)
-        barrier()
+    for _ in range(min(args.steps, 10)):
+        eng.step(timing=timing)
+    barrier()
     eng.check_errors()
     for name in ("interior", "sweep"):  # the roofline kernel: live timings from the timed steps
         if name in live:
@@ -297,7 +407,7 @@ def main() -> int:
         pairs = timing.get(name, [])
         return statistics.mean(a.elapsed_time(z) for a, z in pairs) if pairs else 0.0
 
-    t_ms = max_over_ranks(start.elapsed_time(stop))
+    t_ms = max_over_ranks(t_local)
     sweep_cells = b.cells  # cells the timed TMA launch relaxes
     if (eng.overlap or eng.exchange == "fused") and b.nbr_dirs:
         inner = eng.boxes(b)[0]
@@ -346,6 +456,28 @@ def main() -> int:
     if not args.no_e2e:
         e2e = run_e2e(eng, b, args, world, barrier, max_over_ranks, total_cells)
 
+    # ---- the same steps on the other input (speed must not depend on zeros)
+    alt = None
+    if not args.no_data_alt:
+        other = "random" if args.data == "hotwall" else "hotwall"
+        barrier()
+        if other == "random":
+            eng.fill_random(seed=1)
+        else:
+            eng.reset()
+        barrier()
+        live_a, t_a, clk_a = timed_steps(eng, b, args.steps, args.warmup, barrier, local)
+        eng.check_errors()
+        t_a = max_over_ranks(t_a)
+        name = "interior" if "interior" in live_a else "sweep"
+        k_ms = statistics.mean(x.elapsed_time(y) for x, y in live_a[name])
+        ach = ALG_BYTES_PER_CELL * sweep_cells / (k_ms * 1e-3) / 1e9
+        v_a = total_cells * args.steps / (t_a * 1e-3) / 1e9
+        alt = {"data": data_desc[other], "value": v_a, "unit": UNIT,
+               "ms_per_step": t_a / args.steps, "rel_to_line": v_a / value,
+               "roofline": {"achieved": ach, "peak": peak, "frac": ach / peak, "kernel_ms": k_ms},
+               "clocks": clk_a}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = cpu_sample(args.block, args.cpu_seconds)
@@ -355,7 +487,7 @@ def main() -> int:
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_ms / args.steps,
             "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (Dirichlet hot wall, cl/jacobi3d.py:131-138)",
+            "data": data_desc[args.data],
             "config": {"workload": workload,
                        "global_dims": list(dims), "grid": list(eng.grid), "policy": args.policy,
                        "exchange": eng.exchange if world > 1 else "none (single block)",
@@ -380,11 +512,16 @@ def main() -> int:
                       "isolated_nvlink_frac": (face_bytes / (iso_ms * 1e-3) / 1e9 / NVLINK_GBS)
                       if iso_ms else None} if world > 1 else None),
             "gpu_launches": launches,
-            "clocks": clk.summary(),
+            "clocks": clk,
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "data_alt": alt,
         }
     eng.close()
+    del eng, b
+    torch.cuda.empty_cache()
+    if world == 1 and not args.no_e2e_api and not args.dims:
+        line["e2e_api"] = run_e2e_api(dims, args.steps)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
@@ -393,6 +530,54 @@ def main() -> int:
         line["p2p"] = None if args.no_p2p else p2p_probe()
         print(json.dumps(line), flush=True)
     return 0
+
+
+def timed_steps(eng, b, steps, warmup, barrier, local):
+    """W untimed steps, then K steps bracketed by barrier + synchronize and
+    one CUDA event pair on the block's main stream, nvidia-smi sampling the
+    clocks throughout. The dominant kernel (the interior / full sweep) is
+    timed live inside the timed steps by one event pair per step on its own
+    stream; returns (live kernel events, step time in ms, clock summary)."""
+    import torch
+
+    s = eng.stream_of(b)
+    start, stop = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        for _ in range(warmup):
+            eng.step()
+        barrier()
+        split = (eng.overlap or eng.exchange == "fused") and bool(b.nbr_dirs)
+        live = {"_only": {"interior" if split else "sweep"}}
+        start.record(s)
+        for _ in range(steps):
+            eng.step(timing=live)
+        stop.record(s)
+        barrier()
+    live.pop("_only")
+    return live, start.elapsed_time(stop), clk.summary()
+
+
+def run_e2e_api(dims, iters):
+    """The reference's own entry point, end to end: run_jacobi(dims, iters,
+    mode="channel-persistent") (cl/jacobi3d.py:335-379) — block allocation
+    and Dirichlet init in HBM, the iterations (two eager, the rest replayed
+    from CUDA graphs), and the whole field read back into the returned numpy
+    array. Wall clock around the call."""
+    from paper_2102_12416_b200.jacobi3d import run_jacobi
+
+    t0 = time.perf_counter()
+    r = run_jacobi(dims, iters, mode="channel-persistent", pes=1)
+    wall = time.perf_counter() - t0
+    cells = dims[0] * dims[1] * dims[2]
+    field_bytes = r["field"].nbytes
+    del r["field"]
+    return {"value": cells * iters / wall / 1e9, "unit": UNIT, "wall_s": wall,
+            "iterations_ms_per_iter": r["total_ns"] / iters / 1e6,
+            "iterations_value": cells * iters / (r["total_ns"] * 1e-9) / 1e9,
+            "d2h_bytes": field_bytes, "h2d_bytes": 0, "iters": iters,
+            "api": "paper_2102_12416_b200.jacobi3d.run_jacobi(mode='channel-persistent')",
+            "note": "includes block allocation, init and the one-time read-back of the whole "
+                    "field (the reference's return value); iterations_* is the loop alone"}
 
 
 def p2p_probe() -> dict | None:

@@ -561,15 +561,16 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
     } else if (ok) {  // unaligned bulk or pull
         copy_bytes((char *)dst, from_p, take, tid, nth, true);
     }
-    // no fence before the arrival count: a CTA's slot (or source) reads are
-    // complete once the barrier passed — their values fed stores issued
-    // before it — and that is all the credit promises the sender
-    if (chan_last_cta(c.counter, 2) && threadIdx.x == 0 && ok) {
+    // the credit hands the slot (or the pulled source) back to the sender:
+    // every CTA fences at GPU scope before its arrival count, and the last
+    // CTA publishes with a system-scope release, which is cumulative over
+    // all of them — so by the PTX memory model (not only because the loaded
+    // values fed stores issued before the barrier) every slot read is
+    // performed before the sender can overwrite the slot
+    if (chan_last_cta(c.counter, 0) && threadIdx.x == 0 && ok) {
         chan_stamp(c, k, 3);
         if (len_out) *len_out = len;  // > capacity: the caller reports truncation
-        // every thread's slot reads fed its stores before the barrier, so
-        // the slot may be handed back without a fence
-        st_relaxed_sys(c.credit, k + 1);
+        hx::st_release_sys(c.credit, k + 1);
     }
 }
 

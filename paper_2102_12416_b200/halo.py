@@ -187,6 +187,8 @@ class HaloJacobi:
     path (pack, NCCL send/recv, unpack). overlap applies to "p2p" only.
     """
 
+    e2e_ring_slots = 4096  # device residual slots of step_e2e (zeroed when the ring wraps)
+
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
                  policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False,
                  exchange: str = "fused"):
@@ -243,6 +245,21 @@ class HaloJacobi:
                 b.arena[:_HDR].zero_()
             b.cur = 0
         self.it = 0
+        self.synchronize()
+
+    def fill_random(self, seed: int = 0) -> None:
+        """Seeded N(0,1) interior on both buffers of every local block; the
+        ghost planes keep their Dirichlet values (cl/jacobi3d.py:131-138).
+        Resets the step counter and the channel flags, so the next step
+        re-primes the halo. Collective: every process calls it between two
+        barriers (no step of any block may be in flight)."""
+        self.reset()
+        for b in self.blocks.values():
+            g = torch.Generator(device=f"cuda:{b.device}")
+            g.manual_seed(seed * 1000003 + b.rank)
+            with torch.cuda.device(b.device), torch.cuda.stream(self.stream_of(b)):
+                for f in b.fields:
+                    f[1:-1, 1:-1, 1:-1].normal_(generator=g)
         self.synchronize()
 
     def connect(self) -> None:
@@ -319,7 +336,11 @@ class HaloJacobi:
             return None
         buf = self._res.setdefault(b.rank, [])
         if len(buf) <= it:
-            buf.append(torch.zeros(1, dtype=torch.int64, device=f"cuda:{b.device}"))
+            # zero-filled on the block's main stream: every kernel that
+            # accumulates into the slot is ordered after it (the comm stream
+            # waits on the main stream's `ready` event, recorded later)
+            with torch.cuda.stream(self.stream_of(b)):
+                buf.append(torch.zeros(1, dtype=torch.int64, device=f"cuda:{b.device}"))
         return buf[it].data_ptr()
 
     def step(self, residual=False, timing: dict | None = None) -> None:
@@ -525,6 +546,9 @@ class HaloJacobi:
         blocks = [b for b in self.blocks.values() if devices is None or b.device in devices]
         mark = _Marks(timing)
         shell_done = {}
+        # residual slots first: a new slot is zero-filled on the main stream
+        # before `ready` is recorded, so the shell's atomics follow the fill
+        rps = {b.rank: self._res_ptr(b, it, residual) for b in blocks}
         for b in blocks:
             if not b.nbr_dirs:
                 continue
@@ -544,16 +568,18 @@ class HaloJacobi:
             _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
                       len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array(wait), base + 1,
                       _lib.ptr_array(signal), base + 2, b.counters_ptr + 4, self.timeout_ns,
-                      b.err_ptr, self._res_ptr(b, it, residual),
-                      b.step_ptr if dev_step else None, c.cuda_stream)
+                      b.err_ptr, rps[b.rank], b.step_ptr if dev_step else None, c.cuda_stream)
             mark.end("exchange", b, c)
             ev = torch.cuda.Event()
             ev.record(c)
             shell_done[b.rank] = ev
+        # every local interior is enqueued before any main stream waits for
+        # a shell, so blocks sharing a GPU do not serialise their interiors
+        # behind each other's (spinning) boundary kernels
         for b in blocks:
             _lib.call("hx_set_device", b.device)
             s = self.stream_of(b)
-            rp = self._res_ptr(b, it, residual)
+            rp = rps[b.rank]
             mark.begin("sweep", b, s)
             mark.begin("interior", b, s)
             if b.nbr_dirs:
@@ -563,6 +589,9 @@ class HaloJacobi:
                 _lib.call("hx_stencil", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz,
                           rp, s.cuda_stream)
             mark.end("interior", b, s)
+        for b in blocks:
+            _lib.call("hx_set_device", b.device)
+            s = self.stream_of(b)
             mark.begin("exposed", b, s)
             if b.rank in shell_done:
                 s.wait_event(shell_done[b.rank])
@@ -689,6 +718,13 @@ class HaloJacobi:
             ring = st["ring"][b.rank]
             slot = it % ring.numel()
             if slot == 0:
+                # the ring wraps: the slots are about to be zeroed, so the
+                # reads of every earlier step's residual must have finished.
+                # The read-back stream is in order, so its latest event
+                # covers all of them.
+                last = st["read_done"].get(b.device)
+                if last is not None:
+                    s.wait_event(last)
                 with torch.cuda.stream(s):
                     ring.zero_()
             slots[b.rank] = ring.data_ptr() + 8 * slot
@@ -704,6 +740,9 @@ class HaloJacobi:
                 cs.wait_event(done)        # must not queue behind this sweep
                 _lib.call("hx_memcpy", res_out.data_ptr() + 8 * blocks.index(b), slots[b.rank], 8,
                           cs.cuda_stream)
+                read = torch.cuda.Event()
+                read.record(cs)
+                st["read_done"][b.device] = read
 
     def drain_e2e(self) -> None:
         st = self._e2e_state()
@@ -717,9 +756,10 @@ class HaloJacobi:
             st = self._e2e = {
                 "up": {d: torch.cuda.Stream(device=d) for d in self.streams},
                 "down": {d: torch.cuda.Stream(device=d) for d in self.streams},
-                "ring": {r: torch.zeros(4096, dtype=torch.int64, device=f"cuda:{b.device}")
+                "ring": {r: torch.zeros(self.e2e_ring_slots, dtype=torch.int64,
+                                        device=f"cuda:{b.device}")
                          for r, b in self.blocks.items()},
-                "sweep_done": {}, "uploaded": {},
+                "sweep_done": {}, "uploaded": {}, "read_done": {},
             }
         return st
 

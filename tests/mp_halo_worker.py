@@ -1,6 +1,7 @@
 """torchrun worker for the multi-process (CUDA IPC) halo path.
 
     torchrun --nproc-per-node N tests/mp_halo_worker.py DX DY DZ ITERS OUT.json [MODE]
+    HX_SAME_GPU=1 torchrun ...   (every rank on cuda:0: the 1-GPU IPC variant)
 
 MODE: 0 = channel exchange, 1 = channel exchange + interior overlap,
 fused = boundary sweep stores straight into the neighbours' ghost planes,
@@ -33,10 +34,14 @@ def main():
     out = sys.argv[5]
     mode = sys.argv[6] if len(sys.argv) > 6 else "0"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ["LOCAL_RANK"])
+    # HX_SAME_GPU=1: every rank on cuda:0 — CUDA IPC opens another process's
+    # allocation on the same device, so a 1-GPU box runs the cross-process path
+    same = os.environ.get("HX_SAME_GPU") == "1"
+    local = 0 if same else int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
-    eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=lambda r: r, dist=dist, timeout_s=20,
+    eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=(lambda r: 0) if same else (lambda r: r),
+                     dist=dist, timeout_s=20,
                      overlap=mode == "1", exchange="fused" if mode in ("fused", "graph") else "p2p")
     if mode == "graph":
         eng.run_graph(iters)
