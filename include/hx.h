@@ -70,6 +70,9 @@ int hx_enable_peer(int dev, int peer);               /* idempotent */
 int hx_ipc_get(void *ptr, void *handle_out, size_t *offset_out);
 int hx_ipc_open(const void *handle, void **base_out); /* cached per handle */
 int hx_ipc_close(void *base);
+/* The allocation holding ptr: base address and size (cuMemGetAddressRange);
+ * lets a sender cache one exported IPC handle per allocation. */
+int hx_alloc_range(const void *ptr, void **base_out, size_t *size_out);
 
 /* --------------------------------------------------------------- copies --
  * cl/devicesim.py:197-224 (host_to_device / device_to_host /

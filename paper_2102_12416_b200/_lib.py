@@ -28,7 +28,7 @@ EXPORTS = (
     "hx_stream_synchronize", "hx_event_create", "hx_event_destroy", "hx_event_record",
     "hx_event_query", "hx_event_synchronize", "hx_event_elapsed_ms", "hx_stream_wait_event",
     "hx_malloc", "hx_free", "hx_malloc_host", "hx_free_host", "hx_can_access_peer",
-    "hx_enable_peer", "hx_ipc_get", "hx_ipc_open", "hx_ipc_close", "hx_memcpy",
+    "hx_enable_peer", "hx_ipc_get", "hx_ipc_open", "hx_ipc_close", "hx_alloc_range", "hx_memcpy",
     "hx_memcpy_peer", "hx_copy_sm", "hx_move", "hx_copy_sm_window", "hx_fill_f64", "hx_stencil", "hx_stencil_box",
     "hx_stencil_set_variant", "hx_stencil_last_variant", "hx_stencil_set_chunk", "hx_div6_check",
     "hx_init_block", "hx_pack", "hx_unpack", "hx_pack_put", "hx_wait_unpack", "hx_shell_put",
@@ -87,6 +87,7 @@ _SIGS = {
     "hx_ipc_get": ([_V, _V, ctypes.POINTER(_SZ)], _I),
     "hx_ipc_open": ([_V, ctypes.POINTER(_V)], _I),
     "hx_ipc_close": ([_V], _I),
+    "hx_alloc_range": ([_V, ctypes.POINTER(_V), ctypes.POINTER(_SZ)], _I),
     "hx_memcpy": ([_V, _V, _SZ, _V], _I),
     "hx_memcpy_peer": ([_V, _I, _V, _I, _SZ, _V], _I),
     "hx_copy_sm": ([_V, _V, _SZ, _V], _I),

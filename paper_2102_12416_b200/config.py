@@ -76,6 +76,9 @@ class RuntimeConfig:
     tag_layout: TagLayoutSpec = field(default_factory=TagLayoutSpec)
     gpus: tuple | None = None  # worker -> CUDA ordinal; None = round robin
     flag_timeout_s: float = 30.0  # device-side wait bound (never hang a GPU)
+    # "loopback": every PE in this process; "ipc": one process per GPU under
+    # torch.distributed, PE p in process p % world (transport.TransportGroup)
+    backend: str = "loopback"
 
     def __post_init__(self):
         self.validate()
@@ -89,6 +92,8 @@ class RuntimeConfig:
             raise ConfigError(f"time_mode must be 'wall', got {self.time_mode!r}")
         if self.workers < 1:
             raise ConfigError("workers must be >= 1")
+        if self.backend not in ("loopback", "ipc"):
+            raise ConfigError(f"backend must be 'loopback' or 'ipc', got {self.backend!r}")
 
     def node_of(self, rank: int) -> int:
         return rank // max(1, self.ranks_per_node)

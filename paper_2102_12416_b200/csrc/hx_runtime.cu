@@ -181,6 +181,18 @@ int hx_ipc_get(void *ptr, void *handle_out, size_t *offset_out) {
     return 0;
 }
 
+int hx_alloc_range(const void *ptr, void **base_out, size_t *size_out) {
+    if (!ptr || !base_out || !size_out) return HX_E_INVALID;
+    auto range = (PFN_getAddressRange)hx_internal_driver_sym("cuMemGetAddressRange");
+    if (!range) return HX_E_NODRIVER;
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS) return HX_E_INVALID;
+    *base_out = (void *)base;
+    *size_out = size;
+    return 0;
+}
+
 int hx_ipc_open(const void *handle, void **base_out) {
     if (!handle || !base_out) return HX_E_INVALID;
     std::string key((const char *)handle, sizeof(cudaIpcMemHandle_t));

@@ -22,7 +22,19 @@ What is B200-native (the only place device bytes move):
     copy has completed (cl/transport.py:342-365), and ``idle`` reports
     in-flight GPU copies so the runtime never quiesces early
     (cl/transport.py:372-381, cl/runtime.py:530-542).
-The TCP backend (cl/transport.py:469-586) is out of scope: one box, NVLink.
+Backends: "loopback" — every worker in this process (cl/transport.py's
+loopback); "ipc" — one process per GPU (the paper's setup),
+the B200 form of the reference's TCP backend (cl/transport.py:469-586): the
+workers of other processes are reached over a TCP mesh (wire.Mesh) that
+carries only host frames — eager host payloads, envelopes, and for a device
+payload a rendezvous frame holding the source allocation's CUDA IPC handle
+and offset (the "IPC handles carried in the frames" of SURVEY §8f row 4).
+The receiver opens the handle once (cached), copies straight from the
+sender's HBM into its sink on its own stream, and acknowledges with a FIN
+frame that completes the send. Device payloads never touch a socket or host
+memory. Eager device payloads are snapshotted into a transport-owned bounce
+buffer first (the send completes at once); rendezvous frames leave once the
+source's stream has reached the send (a CUDA event, polled).
 """
 
 from __future__ import annotations
@@ -39,6 +51,10 @@ from .config import RuntimeConfig
 from .device import DeviceBuffer, DeviceRegion, DeviceSpace, as_region
 from .tags import EAGER, FULL_MASK, TagLayout
 from .timebase import WallClock
+from .wire import Mesh
+
+# ipc backend frame kinds (wire.Mesh)
+K_EAGER, K_RTS, K_FIN, K_RUNTIME = 1, 2, 3, 4
 
 
 class TransportError(RuntimeError):
@@ -145,6 +161,10 @@ class Worker:
         self._arrival_seq = 0
         self.hold = None
         self._held: list = []
+        # ipc backend: sends to other processes in order (each waits for its
+        # ready event), and rendezvous sends awaiting the receiver's FIN
+        self._outbox: deque = deque()
+        self._rdv: dict = {}
 
     # ------------------------------------------------------------- plumbing
 
@@ -198,6 +218,9 @@ class Worker:
             raise ValueError(f"payload of {nbytes} bytes exceeds max message size "
                              f"{self.cfg.max_message_bytes}")
         peer = self.group.workers[ep.peer]
+        if isinstance(peer, _RemoteWorker):
+            self._send_remote(peer, tag, source, nbytes, completion)
+            return
         if nbytes <= self.cfg.eager_threshold:
             ready, keep = None, None
             if isinstance(source, DeviceRegion):
@@ -229,6 +252,56 @@ class Worker:
         self.stats[_TX_KEY[frame.kind]] += 1
         self.stats["sends"] += 1
         peer.inbound.append(frame)
+
+    def _send_remote(self, peer, tag, source, nbytes, completion) -> None:
+        """ipc backend: a send to a worker of another process. Host bytes go
+        as an eager frame (the send completes at once); a device payload goes
+        as a rendezvous frame carrying the source's IPC handle — eager-sized
+        ones from a bounce snapshot (send complete at once, the bounce comes
+        back with the FIN), larger ones straight from the source region (the
+        FIN completes the send). Frames leave in send order."""
+        self.stats["sends"] += 1
+        if isinstance(source, bytes):
+            self.stats["tx_eager"] += 1
+            self._outbox.append((None, self.group.process_of(peer.id),
+                                 (K_EAGER, (peer.id, self.id, tag, source))))
+            self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
+            self._flush_outbox()
+            return
+        sid = self.group.next_sid()
+        if nbytes <= self.cfg.eager_threshold:
+            self.stats["tx_eager"] += 1
+            snap, ready, keep = self._snapshot(source)
+            self._fire(completion, Completion(status=OK, length=nbytes, tag=tag))
+            self._rdv[sid] = (None, tag, keep)
+            addr = snap.addr
+        else:
+            self.stats["tx_rts"] += 1
+            ready = self.space.record(source.buffer.owner)
+            self._rdv[sid] = (completion, tag, None)
+            addr = source.addr
+        self._outbox.append((ready, self.group.process_of(peer.id),
+                             (K_RTS, [peer.id, self.id, tag, nbytes, addr, sid])))
+        self._flush_outbox()
+
+    def _flush_outbox(self) -> None:
+        while self._outbox:
+            ready, proc_peer, (kind, body) = self._outbox[0]
+            if ready is not None:
+                if not ready.done():
+                    return
+                ready.release()
+                handle, off = self.group.ipc_export(body[4])
+                body = (body[0], body[1], body[2], body[3], handle, off, body[5])
+            self._outbox.popleft()
+            self.group.emit(proc_peer, kind, body)
+
+    def _on_fin(self, sid: int, status: str, length: int, error) -> None:
+        completion, tag, keep = self._rdv.pop(sid)
+        if keep is not None:
+            self.space.return_bounce(keep)
+        if completion is not None:
+            self._fire(completion, Completion(status=status, length=length, tag=tag, error=error))
 
     def _match_now(self, frame: Frame) -> bool:
         """Receiver side of a direct send: if a posted receive matches and no
@@ -284,6 +357,10 @@ class Worker:
 
     def progress(self) -> int:
         """Drain arrivals, poll GPU copies, fire completions (cl/transport.py:342-362)."""
+        if self.group.mesh is not None:
+            self.group.poll()
+            if self._outbox:
+                self._flush_outbox()
         while self.inbound:
             frame = self.inbound.popleft()
             if self.hold is not None and self.hold(frame):
@@ -317,7 +394,7 @@ class Worker:
     @property
     def idle(self) -> bool:
         """No arrivals, completions, or in-flight GPU copies."""
-        return not (self.inbound or self._fired or self._inflight)
+        return not (self.inbound or self._fired or self._inflight or self._outbox or self._rdv)
 
     def _arrived(self, frame: Frame) -> None:
         frame.seq = self._arrival_seq
@@ -448,7 +525,7 @@ class Worker:
         return ev
 
     def _d2h(self, src, n: int, ready):
-        owner = src.owner if isinstance(src, _Bounce) else src.buffer.owner
+        owner = src.buffer.owner if isinstance(src, DeviceRegion) else src.owner
         h = self.space.handle_of(owner)
         if ready is not None:
             ready.wait_on(h)
@@ -475,26 +552,161 @@ class _Bounce:
         self.owner = owner
 
 
+class _RemoteRegion:
+    """A device payload living in another process's HBM, named by its
+    allocation's CUDA IPC handle and offset; mapped (once per handle) into
+    this process on first use."""
+
+    __slots__ = ("group", "handle", "offset", "size", "owner", "_addr")
+
+    def __init__(self, group, handle, offset, size, owner):
+        self.group, self.handle, self.offset, self.size, self.owner = group, handle, offset, size, owner
+        self._addr = None
+
+    @property
+    def addr(self) -> int:
+        if self._addr is None:
+            self._addr = self.group.ipc_open(self.handle, self.group.gpu_of(self.owner)) + self.offset
+        return self._addr
+
+
+class _FinToken:
+    """Send completion of a remote rendezvous: firing it emits the FIN."""
+
+    __slots__ = ("proc", "worker", "sid")
+
+    def __init__(self, proc, worker, sid):
+        self.proc, self.worker, self.sid = proc, worker, sid
+
+
+class _RemoteWorker:
+    """Stand-in for a worker of another process (ipc backend): what a local
+    receiver does to "the sender" — fire its send completion, keep it busy —
+    becomes a FIN frame, or nothing."""
+
+    def __init__(self, group, worker_id: int):
+        self.group = group
+        self.id = worker_id
+
+    def _fire(self, handle, comp: Completion) -> None:
+        if isinstance(handle, _FinToken):
+            self.group.emit(handle.proc, K_FIN, (handle.worker, handle.sid, comp.status,
+                                                 comp.length, comp.error))
+
+    def _after(self, event, fn) -> None:
+        pass
+
+
 class TransportGroup:
     """Process-local workers, wall clocks and the HBM device space
     (cl/transport.py:601-636). Enables NVLink peer access between every
-    pair of GPUs the workers use."""
+    pair of GPUs the workers use.
+
+    backend "ipc": one process per GPU under an initialised
+    torch.distributed process group; worker w lives in process
+    ``w % world`` (process_of). The other processes' workers appear as
+    _RemoteWorker stand-ins, and the group owns the TCP mesh, the IPC handle
+    caches (exported and opened) and the dispatch of arriving frames."""
 
     def __init__(self, cfg: RuntimeConfig | None = None, backend: str = "loopback"):
-        if backend != "loopback":
-            raise StartupError(f"backend {backend!r} is out of scope on the B200 path "
-                               "(single box, NVLink); use 'loopback'")
+        if backend not in ("loopback", "ipc"):
+            raise StartupError(f"unknown backend {backend!r} (the B200 path offers 'loopback' "
+                               "and 'ipc': one process per GPU, CUDA IPC data plane)")
         self.cfg = cfg or RuntimeConfig()
         self.backend = backend
         self.layout = TagLayout.from_spec(self.cfg.tag_layout)
-        self.workers: dict[int, Worker] = {}
+        self.workers: dict = {}
         self.clocks: dict[int, WallClock] = {}
         self._device_space: DeviceSpace | None = None
         self._ngpu = None
+        self.rank, self.world = 0, 1
+        self.mesh = None
+        self.runtime_handler = None  # ipc: callback(obj) for runtime frames
+        self._sid = 0
+        self._exported: dict = {}
+        self._opened: dict = {}
+        if backend == "ipc":
+            import torch.distributed as dist
+
+            if not dist.is_initialized():
+                raise StartupError("backend 'ipc' needs an initialised torch.distributed process "
+                                   "group (one process per GPU, e.g. under torchrun)")
+            self.rank, self.world = dist.get_rank(), dist.get_world_size()
+            self.mesh = Mesh(self.rank, self.world, self.layout.digest(), dist,
+                             timeout_s=max(self.cfg.connect_timeout_s, 30.0))
+            for w in range(self.cfg.workers):
+                if not self.is_local(w):
+                    self.workers[w] = _RemoteWorker(self, w)
+
+    # ------------------------------------------------------------ ipc --
+
+    def process_of(self, worker: int) -> int:
+        return worker % self.world
+
+    def is_local(self, worker: int) -> bool:
+        return self.process_of(worker) == self.rank
+
+    def local_workers(self) -> list:
+        return [w for w in range(self.cfg.workers) if self.is_local(w)]
+
+    def next_sid(self) -> int:
+        self._sid += 1
+        return self._sid
+
+    def emit(self, proc: int, kind: int, body) -> None:
+        self.mesh.send(proc, kind, body)
+
+    def ipc_export(self, addr: int):
+        """(IPC handle bytes, offset) of the allocation holding ``addr``,
+        cached per allocation base."""
+        b, n = ctypes.c_void_p(), ctypes.c_size_t(0)
+        _lib.call("hx_alloc_range", addr, ctypes.byref(b), ctypes.byref(n))
+        handle = self._exported.get((b.value, n.value))
+        if handle is None:
+            h = (ctypes.c_char * 64)()
+            off = ctypes.c_size_t(0)
+            _lib.call("hx_ipc_get", addr, h, ctypes.byref(off))
+            handle = self._exported[(b.value, n.value)] = bytes(h)
+        return handle, addr - b.value
+
+    def ipc_open(self, handle: bytes, gpu: int) -> int:
+        key = (handle, gpu)
+        base = self._opened.get(key)
+        if base is None:
+            p = ctypes.c_void_p()
+            _lib.call("hx_set_device", gpu)
+            _lib.call("hx_ipc_open", handle, ctypes.byref(p))
+            base = self._opened[key] = p.value
+        return base
+
+    def poll(self) -> None:
+        """Deliver every frame that has arrived from the other processes."""
+        for proc, kind, body in self.mesh.poll():
+            if kind == K_EAGER:
+                dst, src, tag, data = body
+                self.workers[dst].inbound.append(
+                    Frame(FRAME_EAGER, tag, len(data), data, None, src))
+            elif kind == K_RTS:
+                dst, src, tag, n, handle, off, sid = body
+                region = _RemoteRegion(self, handle, off, n, dst)
+                self.workers[dst].inbound.append(
+                    Frame(FRAME_RTS, tag, n, region, None, src,
+                          send_completion=_FinToken(proc, src, sid)))
+            elif kind == K_FIN:
+                worker, sid, status, length, error = body
+                self.workers[worker]._on_fin(sid, status, length, error)
+            elif kind == K_RUNTIME:
+                if self.runtime_handler is None:
+                    raise TransportError("runtime frame arrived but no runtime is attached")
+                self.runtime_handler(body)
+            else:
+                raise TransportError(f"unknown frame kind {kind} from process {proc}")
 
     def gpu_of(self, worker: int) -> int:
         if self.cfg.gpus:
             return int(self.cfg.gpus[worker % len(self.cfg.gpus)])
+        if self.backend == "ipc":
+            return torch.cuda.current_device()  # one process per GPU
         if self._ngpu is None:
             self._ngpu = max(1, torch.cuda.device_count())
         return worker % self._ngpu
@@ -502,6 +714,9 @@ class TransportGroup:
     def create_worker(self, worker_id: int, listen: str | None = None) -> Worker:
         if worker_id in self.workers:
             raise StartupError(f"duplicate worker id {worker_id} in process group")
+        if not self.is_local(worker_id):
+            raise StartupError(f"worker {worker_id} belongs to process "
+                               f"{self.process_of(worker_id)}, not {self.rank}")
         self.clocks[worker_id] = WallClock()
         w = Worker(self, worker_id)
         self.workers[worker_id] = w
@@ -511,7 +726,8 @@ class TransportGroup:
     def device_space(self) -> DeviceSpace:
         if self._device_space is None:
             self._device_space = DeviceSpace(self.gpu_of, self.clocks, self.cfg.device_capacity)
-            gpus = sorted({self.gpu_of(w) for w in range(max(self.cfg.workers, 1))})
+            gpus = sorted({self.gpu_of(w) for w in range(max(self.cfg.workers, 1))
+                           if self.is_local(w)})
             for a in gpus:
                 for b in gpus:
                     if a != b:
@@ -525,3 +741,9 @@ class TransportGroup:
         if self._device_space is not None:
             for s in self._device_space._streams.values():
                 s.synchronize()
+        for base in self._opened.values():
+            _lib.raw("hx_ipc_close")(base)
+        self._opened.clear()
+        if self.mesh is not None:
+            self.mesh.close()
+            self.mesh = None
