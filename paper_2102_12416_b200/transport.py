@@ -40,6 +40,7 @@ source's stream has reached the send (a CUDA event, polled).
 from __future__ import annotations
 
 import ctypes
+import weakref
 from collections import Counter, deque
 
 import numpy as np
@@ -608,7 +609,10 @@ class TransportGroup:
     _RemoteWorker stand-ins, and the group owns the TCP mesh, the IPC handle
     caches (exported and opened) and the dispatch of arriving frames."""
 
+    _live = weakref.WeakSet()  # diagnostics: debug_state() of every open group
+
     def __init__(self, cfg: RuntimeConfig | None = None, backend: str = "loopback"):
+        TransportGroup._live.add(self)
         if backend not in ("loopback", "ipc"):
             raise StartupError(f"unknown backend {backend!r} (the B200 path offers 'loopback' "
                                "and 'ipc': one process per GPU, CUDA IPC data plane)")
@@ -637,6 +641,20 @@ class TransportGroup:
             for w in range(self.cfg.workers):
                 if not self.is_local(w):
                     self.workers[w] = _RemoteWorker(self, w)
+
+    def debug_state(self) -> dict:
+        """Queue depths of every local worker (diagnosing a stalled run)."""
+        out = {"rank": self.rank, "world": self.world}
+        for w, wk in self.workers.items():
+            if isinstance(wk, Worker):
+                out[w] = {"posted": [hex(r.tag) for r in wk.posted][:8],
+                          "unexpected": [repr(f) for f in wk.unexpected][:8],
+                          "inbound": len(wk.inbound), "fired": len(wk._fired),
+                          "inflight": len(wk._inflight), "outbox": len(wk._outbox),
+                          "rdv": sorted(wk._rdv)[:8], "stats": dict(wk.stats)}
+        if self.mesh is not None:
+            out["mesh"] = {p: (len(c.wbuf), len(c.rbuf), c.closed) for p, c in self.mesh.conns.items()}
+        return out
 
     # ------------------------------------------------------------ ipc --
 

@@ -15,6 +15,7 @@ PE p runs in process p % 2. Checked, bit for bit / byte for byte:
 Rank 0 writes {"ok": bool, "failures": [...], "osu": [...]} to OUT.json.
 """
 
+import faulthandler
 import hashlib
 import json
 import os
@@ -33,6 +34,15 @@ def main():
     from paper_2102_12416_b200.config import RuntimeConfig
     from paper_2102_12416_b200.jacobi3d import ALL_MODES, run_jacobi
 
+    import signal
+
+    from paper_2102_12416_b200.transport import TransportGroup
+
+    def dump(signum, frame):  # a stalled case prints every open group's queues
+        for g in list(TransportGroup._live):
+            print(f"[{dist.get_rank()}] STALL {g.debug_state()}", flush=True)
+
+    signal.signal(signal.SIGALRM, dump)
     out = sys.argv[1]
     quick = len(sys.argv) > 2 and sys.argv[2] == "quick"
     same = os.environ.get("HX_SAME_GPU") == "1"
@@ -52,6 +62,10 @@ def main():
         cases.append(((64, 64, 64), 100, 2, gold["seq_64_100"]["sha256"]))
     for dims, iters, pes, want in cases:
         for mode in ALL_MODES:
+            # a hung case dumps every thread's stack and exits (never a silent hang)
+            faulthandler.dump_traceback_later(120, exit=True)
+            signal.alarm(100)
+            print(f"[{rank}] run_jacobi {dims} x {iters} {mode} pes={pes}", flush=True)
             try:
                 r = run_jacobi(dims, iters, mode, pes, cfg=cfg)
                 if sha(r["field"]) != want:
@@ -68,6 +82,9 @@ def main():
     for api in osu.APIS:
         for mode in osu.MODES:
             for size in sizes:
+                faulthandler.dump_traceback_later(120, exit=True)
+                signal.alarm(100)
+                print(f"[{rank}] osu {api}/{mode}/{size}", flush=True)
                 try:
                     lat = osu.measure_latency(api, mode, size, iters=10, warmup=2, cfg=bcfg)
                     bw = osu.measure_bandwidth(api, mode, size, window=8, iters=2, cfg=bcfg)
@@ -81,6 +98,8 @@ def main():
                 except Exception as e:  # noqa: BLE001
                     failures.append(f"osu {api}/{mode}/{size}: {type(e).__name__}: {e}")
 
+    faulthandler.cancel_dump_traceback_later()
+    signal.alarm(0)
     everyone = [None] * dist.get_world_size()
     dist.all_gather_object(everyone, failures)
     if rank == 0:
