@@ -606,6 +606,166 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
     }
 }
 
+// ------------------------------------------- TMA boundary faces -------
+// The fused exchange for x and y face slabs (the shell of every benchmark
+// decomposition without a z split). A face tile is FR rows x FK columns;
+// one TMA box brings its three layers (the face and its two neighbours
+// along the normal) with a one-cell halo into shared memory. Persistent
+// CTAs walk their tiles through an FNST-stage ring, so the loads of the
+// next tiles are in flight while 8 warps relax the current one (one tile
+// row each, 4 cells per lane, 32 consecutive k per store) and store it
+// locally and straight into the neighbour's ghost plane over NVLink. The
+// per-row kernel above issues six dependent global loads per cell and is
+// latency-bound (16 % warps active, profiles/r1_exchange_kernels.md).
+constexpr int FR = 8;                 // tile rows across the face (one warp each)
+constexpr int FK = 128;               // tile columns (k): 4 x 32 lanes
+constexpr int FBK = FK + 2;           // box width: k-1 .. k+FK (1040 B, a 16-byte multiple)
+constexpr int FBR = FR + 2;           // box rows across the face, with the row halo
+constexpr int FNST = 2;               // ring stages (3 CTAs/SM)
+constexpr unsigned FACE_BYTES = 3u * FBR * FBK * sizeof(double);
+constexpr unsigned FACE_STRIDE = (FACE_BYTES + 127u) / 128u * 128u;
+constexpr size_t FACE_SMEM = (size_t)FNST * FACE_STRIDE + FNST * sizeof(uint64_t);
+
+struct FaceJob {
+    int nbox;
+    int axis[4];   // 0: x slab (plane i = pos), 1: y slab (row j = pos)
+    int pos[4];
+    int lo[4], hi[4];  // rows across the face: j (x slab) or i (y slab), 1-based, half-open
+    int k0, k1;
+    int tiles[5];  // prefix tile counts
+    int ntk;
+    double *remote[6];
+    long long shift[6];
+    int face[6];
+    unsigned long long *wait[6];
+    unsigned long long *signal[6];
+};
+
+__global__ void __launch_bounds__(256)
+face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy,
+                double *__restrict__ nxt, int by, int bz, FaceJob J,
+                unsigned long long wait_value, unsigned long long signal_value, unsigned *counter,
+                unsigned long long timeout_ns, int *err, unsigned long long *res,
+                unsigned long long *step) {
+    extern __shared__ __align__(128) unsigned char smem[];
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + FNST * FACE_STRIDE);
+    __shared__ int ok;
+    __shared__ unsigned long long base;
+    const int total = J.tiles[J.nbox];
+    const int count = ((int)blockIdx.x < total) ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // thread 0: the TMA box of this CTA's n-th tile into stage s
+    auto load = [&](int n, int s) {
+        const int t = (int)blockIdx.x + n * (int)gridDim.x;
+        int b = 0;
+        while (t >= J.tiles[b + 1]) ++b;
+        const int lt = t - J.tiles[b];
+        const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = J.k0 + (lt % J.ntk) * FK;
+        hx::mbar_expect_tx(&bar[s], FACE_BYTES);
+        if (J.axis[b] == 0)
+            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapx, kb - 1, r0 - 1, J.pos[b] - 1, &bar[s]);
+        else
+            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapy, kb - 1, J.pos[b] - 1, r0 - 1, &bar[s]);
+    };
+    if (threadIdx.x == 0) {
+        base = step ? *(volatile unsigned long long *)step : 0ull;
+        ok = 1;
+        for (int d = 0; d < 6 && ok; ++d)
+            if (J.wait[d]) ok = hx::spin_until(J.wait[d], base + wait_value, timeout_ns, err);
+        // the ghost layers were stored by the peers (generic proxy, made
+        // visible by the acquire): order them before the TMA's reads
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        if (ok && count) {
+            hx::prefetch_tmap(&mapx);
+            hx::prefetch_tmap(&mapy);
+            for (int s = 0; s < FNST; ++s) hx::mbar_init(&bar[s], 1);
+            hx::fence_mbar_init();
+            for (int n = 0; n < FNST && n < count; ++n) load(n, n);
+        }
+    }
+    __syncthreads();
+    unsigned long long worst = 0;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const size_t pz = (size_t)bz + 2;
+    for (int n = 0; ok && n < count; ++n) {
+        const int s = n % FNST;
+        const int t = (int)blockIdx.x + n * (int)gridDim.x;
+        int b = 0;
+        while (t >= J.tiles[b + 1]) ++b;
+        const int lt = t - J.tiles[b];
+        const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = J.k0 + (lt % J.ntk) * FK;
+        const bool xs = J.axis[b] == 0;
+        const int row = r0 + w;
+        const int i = xs ? J.pos[b] : row, j = xs ? row : J.pos[b];
+        // this row's destinations: our nxt, and the ghost plane of every
+        // neighbour whose face the row lies on (the slab's own face, plus a
+        // y face on an x slab's edge rows); no z neighbour on this path
+        const long long crow = ((long long)i * (by + 2) + j) * (long long)pz + kb;
+        double *dst = nxt + crow;
+        double *rd0 = nullptr, *rd1 = nullptr;
+#pragma unroll
+        for (int d = 0; d < 4; ++d)
+            if (J.remote[d] && (d < 2 ? i : j) == J.face[d]) {
+                double *r = J.remote[d] + (crow + J.shift[d]);
+                if (!rd0) rd0 = r; else rd1 = r;
+            }
+        // shared-memory strides: x slab S[3][FBR][FBK], y slab S[FBR][3][FBK]
+        const int ssx = xs ? FBR * FBK : 3 * FBK;
+        const int C0 = (xs ? (FBR + w + 1) : (3 * (w + 1) + 1)) * FBK + 1 + lane;
+        const int nk = row < J.hi[b] ? min(FK, J.k1 - kb) : 0;  // live columns of this row
+        hx::mbar_wait(&bar[s], (n / FNST) & 1);
+        const double *S = reinterpret_cast<const double *>(smem + s * FACE_STRIDE);
+        constexpr int U = FK / 32;
+        double v[U];
+        bool fast = true;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int C = C0 + 32 * u;
+            v[u] = sum6(S[C - ssx], S[C + ssx], S[C - FBK], S[C + FBK], S[C - 1], S[C + 1]);
+            fast &= div6_fast_ok(v[u]);
+        }
+        if (fast) {
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = div6_fast(v[u]);
+        } else {
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = div6(v[u]);
+        }
+        if (res) {
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (lane + 32 * u < nk) worst = max(worst, abs_diff_bits(v[u], S[C0 + 32 * u]));
+        }
+        // every shared load has completed once the barrier is passed: each
+        // value fed v, and the residual's centre loads feed the predicate
+        (void)__syncthreads_or(res ? (int)(worst >> 63) : (int)(v[0] != v[0]));
+        if (threadIdx.x == 0 && n + FNST < count) load(n + FNST, s);  // refill during the stores
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int kk = lane + 32 * u;
+            if (kk >= nk) continue;
+            dst[kk] = v[u];
+            if (rd0) rd0[kk] = v[u];
+            if (rd1) rd1[kk] = v[u];
+        }
+    }
+    if (res) warp_max_to_global(worst, res);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // as shell_put_kernel: GPU-scope fence and arrival count per CTA, the
+        // last CTA's system fence + releases are cumulative over all of them
+        __threadfence();
+        const unsigned done = atomicAdd(counter, 1u) + 1u;
+        if (done == gridDim.x) {
+            *counter = 0u;
+            __threadfence_system();
+            const bool healthy = !err || *(volatile int *)err == 0;
+            for (int d = 0; d < 6 && healthy; ++d)
+                if (J.signal[d]) hx::st_release_sys(J.signal[d], base + signal_value);
+            if (step) *step = base + 1;
+        }
+    }
+}
+
 __global__ void fill_kernel(double *p, size_t n, double v) {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
          q += (size_t)gridDim.x * blockDim.x)
@@ -655,6 +815,40 @@ int tensor_map_for(const double *cur, int bx, int by, int bz, int box_z, CUtenso
     std::lock_guard<std::mutex> lk(g_map_mu);
     if (g_maps.size() > 256) g_maps.clear();
     g_maps[key] = m;
+    *out = m;
+    return 0;
+}
+
+// Tensor map over the padded block with an arbitrary 3-D box (the face
+// kernel's x-slab and y-slab boxes), cached like tensor_map_for's.
+std::map<std::tuple<const void *, int, int, int, int, int, int>, CUtensorMap> g_face_maps;
+
+int face_map_for(const double *cur, int bx, int by, int bz, int b0, int b1, int b2,
+                 CUtensorMap *out) {
+    auto key = std::make_tuple((const void *)cur, bx, by, bz, b0, b1, b2);
+    {
+        std::lock_guard<std::mutex> lk(g_map_mu);
+        auto it = g_face_maps.find(key);
+        if (it != g_face_maps.end()) {
+            *out = it->second;
+            return 0;
+        }
+    }
+    auto encode = (PFN_cuTensorMapEncodeTiled_v12000)hx_internal_driver_sym("cuTensorMapEncodeTiled");
+    if (!encode) return HX_E_NODRIVER;
+    const cuuint64_t pz = (cuuint64_t)bz + 2, py = (cuuint64_t)by + 2, px = (cuuint64_t)bx + 2;
+    cuuint64_t dims[3] = {pz, py, px};
+    cuuint64_t strides[2] = {pz * sizeof(double), py * pz * sizeof(double)};
+    cuuint32_t box[3] = {(cuuint32_t)b0, (cuuint32_t)b1, (cuuint32_t)b2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUtensorMap m;
+    CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)cur, dims, strides, box,
+                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return HX_E_TMA;
+    std::lock_guard<std::mutex> lk(g_map_mu);
+    if (g_face_maps.size() > 256) g_face_maps.clear();
+    g_face_maps[key] = m;
     *out = m;
     return 0;
 }
@@ -995,6 +1189,7 @@ int hx_preload_halo_kernels();  // hx_halo.cu
 int hx_preload() {
     cudaFuncAttributes a;
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)shell_put_kernel));
+    HX_TRY(cudaFuncGetAttributes(&a, (const void *)face_tma_kernel));
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)fill_kernel));
     return hx_preload_halo_kernels();
 }
@@ -1037,6 +1232,67 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         J.rows[J.nbox + 1] = J.rows[J.nbox] + (int)rows;
         n += (long long)ni * nj * nk;
         ++J.nbox;
+    }
+    // x / y face slabs only (no z column) on a TMA-describable block: the
+    // face kernel (HX_SHELL_FACE_TMA=0 keeps the per-row kernel, for A/B)
+    static int face_tma = -1;
+    if (face_tma < 0) {
+        const char *e = getenv("HX_SHELL_FACE_TMA");
+        face_tma = e ? atoi(e) : 1;
+    }
+    bool faces_only = face_tma && J.nbox > 0 && J.nbox <= 4 && tma_eligible(cur, bz) &&
+                      ((uintptr_t)nxt & 15) == 0 && !J.remote[4] && !J.remote[5] &&
+                      bx >= 2 && by >= 2;  // a row then lies on at most two neighbour faces
+    for (int q = 0; q < J.nbox && faces_only; ++q) {
+        const int *x = J.box[q];
+        const bool xslab = x[1] - x[0] == 1 && x[5] - x[4] > 1;
+        const bool yslab = x[3] - x[2] == 1 && x[1] - x[0] > 1 && x[5] - x[4] > 1;
+        faces_only = (xslab || yslab) && x[4] == J.box[0][4] && x[5] == J.box[0][5];
+    }
+    if (faces_only) {
+        FaceJob F;
+        memset(&F, 0, sizeof(F));
+        F.nbox = J.nbox;
+        F.k0 = J.box[0][4];
+        F.k1 = J.box[0][5];
+        F.ntk = (F.k1 - F.k0 + FK - 1) / FK;
+        F.tiles[0] = 0;
+        for (int q = 0; q < J.nbox; ++q) {
+            const int *x = J.box[q];
+            const bool xslab = x[1] - x[0] == 1;
+            F.axis[q] = xslab ? 0 : 1;
+            F.pos[q] = xslab ? x[0] : x[2];
+            F.lo[q] = xslab ? x[2] : x[0];
+            F.hi[q] = xslab ? x[3] : x[1];
+            const long long t = (long long)((F.hi[q] - F.lo[q] + FR - 1) / FR) * F.ntk;
+            if (F.tiles[q] + t > 0x7fffffffLL) return HX_E_INVALID;
+            F.tiles[q + 1] = F.tiles[q] + (int)t;
+        }
+        for (int d = 0; d < 6; ++d) {
+            F.remote[d] = J.remote[d];
+            F.shift[d] = J.shift[d];
+            F.face[d] = J.face[d];
+            F.wait[d] = J.wait[d];
+            F.signal[d] = J.signal[d];
+        }
+        CUtensorMap mx, my;
+        if (int rc = face_map_for(cur, bx, by, bz, FBK, FBR, 3, &mx)) return rc;
+        if (int rc = face_map_for(cur, bx, by, bz, FBK, 3, FBR, &my)) return rc;
+        static unsigned long long attr_set = 0;
+        if (int rc = ensure_smem(face_tma_kernel, FACE_SMEM, attr_set)) return rc;
+        static int fmult = 0;
+        if (!fmult) {
+            const char *e = getenv("HX_FACE_GRID_MULT");  // persistent CTAs per SM (tuning)
+            fmult = e && atoi(e) > 0 ? atoi(e) : 3;
+        }
+        const unsigned grid = (unsigned)std::max(1, std::min(F.tiles[F.nbox], fmult * num_sms()));
+        if (F.tiles[F.nbox] > 0) {
+            face_tma_kernel<<<grid, 256, FACE_SMEM, (cudaStream_t)stream>>>(
+                mx, my, nxt, by, bz, F, wait_value, signal_value, counter, timeout_ns, err, res,
+                step);
+            HX_LAUNCH_CHECK();
+            return 0;
+        }
     }
     static int mult = 0;
     if (!mult) {

@@ -615,17 +615,20 @@ class HaloJacobi:
         flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
         nxt = b.cur ^ 1
         remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
+        args = (b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz, len(shells), flat,
+                _lib.ptr_array(remote), _lib.ptr_array([None] * 6), 0, _lib.ptr_array([None] * 6),
+                0, b.counters_ptr + 4, self.timeout_ns, b.err_ptr, None, None, c.cuda_stream)
+        _lib.call("hx_shell_put", *args)  # warm (tensor maps, attributes)
         times = []
+        back_to_back = 8  # launches per timing: the host's submit cost stays off the clock
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(c)
-            _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
-                      len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array([None] * 6), 0,
-                      _lib.ptr_array([None] * 6), 0, b.counters_ptr + 4, self.timeout_ns,
-                      b.err_ptr, None, None, c.cuda_stream)
+            for _ in range(back_to_back):
+                _lib.call("hx_shell_put", *args)
             e1.record(c)
             c.synchronize()
-            times.append(e0.elapsed_time(e1))
+            times.append(e0.elapsed_time(e1) / back_to_back)
         return sorted(times)[len(times) // 2]
 
     def run_graph(self, iters: int) -> None:

@@ -5,7 +5,9 @@
 
 MODE: 0 = channel exchange, 1 = channel exchange + interior overlap,
 fused = boundary sweep stores straight into the neighbours' ghost planes,
-graph = fused, replayed from per-process CUDA graphs (no residuals).
+graph = fused, replayed from per-process CUDA graphs (no residuals),
+nccl = the comparison path (pack, grouped NCCL send/recv, unpack; needs one
+GPU per rank — NCCL refuses two ranks on one device).
 
 One rank per GPU: HaloJacobi with local_ranks=[rank] opens its neighbours'
 receive arenas through CUDA IPC handles exchanged once over gloo, runs
@@ -39,10 +41,13 @@ def main():
     same = os.environ.get("HX_SAME_GPU") == "1"
     local = 0 if same else int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
-    dist.init_process_group("gloo")
+    if mode == "nccl":  # the comparison exchange: NCCL send/recv on CUDA tensors, gloo for objects
+        dist.init_process_group("cpu:gloo,cuda:nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group("gloo")
+    exchange = {"fused": "fused", "graph": "fused", "nccl": "nccl"}.get(mode, "p2p")
     eng = HaloJacobi(dims, world, local_ranks=[rank], device_of=(lambda r: 0) if same else (lambda r: r),
-                     dist=dist, timeout_s=20,
-                     overlap=mode == "1", exchange="fused" if mode in ("fused", "graph") else "p2p")
+                     dist=dist, timeout_s=20, overlap=mode == "1", exchange=exchange)
     if mode == "graph":
         eng.run_graph(iters)
     else:

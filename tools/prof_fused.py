@@ -58,13 +58,14 @@ def main():
                           else None for d in range(NDIRS)]
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(c)
-                _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
-                          len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array([None] * 6), 0,
-                          _lib.ptr_array([None] * 6), 0, b.counters_ptr + 4, eng.timeout_ns,
-                          b.err_ptr, None, None, c.cuda_stream)
+                for _ in range(8):  # back to back: the host's submit cost stays off the clock
+                    _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
+                              len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array([None] * 6),
+                              0, _lib.ptr_array([None] * 6), 0, b.counters_ptr + 4, eng.timeout_ns,
+                              b.err_ptr, None, None, c.cuda_stream)
                 e1.record(c)
                 c.synchronize()
-                iso.append(e0.elapsed_time(e1))
+                iso.append(e0.elapsed_time(e1) / 8)
         b = eng.blocks[0]
         cells = sum((x[1] - x[0]) * (x[3] - x[2]) * (x[5] - x[4]) for x in eng.boxes(b)[1])
         face = b.by * b.bz
