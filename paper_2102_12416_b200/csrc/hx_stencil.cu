@@ -619,12 +619,13 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
 // latency-bound (16 % warps active, profiles/r1_exchange_kernels.md).
 constexpr int FR = 8;                 // tile rows across the face (one warp each)
 constexpr int FK = 128;               // tile columns (k): 4 x 32 lanes
-constexpr int FBK = FK + 2;           // box width: k-1 .. k+FK (1040 B, a 16-byte multiple)
+constexpr int FBK = FK + 4;           // box width: k-2 .. k+FK+1 (1056 B, a 16-byte multiple)
 constexpr int FBR = FR + 2;           // box rows across the face, with the row halo
 constexpr int FNST = 2;               // ring stages (3 CTAs/SM)
 constexpr unsigned FACE_BYTES = 3u * FBR * FBK * sizeof(double);
 constexpr unsigned FACE_STRIDE = (FACE_BYTES + 127u) / 128u * 128u;
-constexpr size_t FACE_SMEM = (size_t)FNST * FACE_STRIDE + FNST * sizeof(uint64_t);
+constexpr unsigned FACE_STAGE_OUT = 8u * FK * sizeof(double);  // one result row per warp
+constexpr size_t FACE_SMEM = (size_t)FNST * FACE_STRIDE + FACE_STAGE_OUT + FNST * sizeof(uint64_t);
 
 struct FaceJob {
     int nbox;
@@ -643,12 +644,13 @@ struct FaceJob {
 
 __global__ void __launch_bounds__(256)
 face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy,
-                double *__restrict__ nxt, int by, int bz, FaceJob J,
+                double *__restrict__ nxt, int by, int bz, FaceJob J, int bulk,
                 unsigned long long wait_value, unsigned long long signal_value, unsigned *counter,
                 unsigned long long timeout_ns, int *err, unsigned long long *res,
                 unsigned long long *step) {
     extern __shared__ __align__(128) unsigned char smem[];
-    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + FNST * FACE_STRIDE);
+    double *outrow = reinterpret_cast<double *>(smem + FNST * FACE_STRIDE);  // [8][FK]
+    uint64_t *bar = reinterpret_cast<uint64_t *>(smem + FNST * FACE_STRIDE + FACE_STAGE_OUT);
     __shared__ int ok;
     __shared__ unsigned long long base;
     const int total = J.tiles[J.nbox];
@@ -659,12 +661,15 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         int b = 0;
         while (t >= J.tiles[b + 1]) ++b;
         const int lt = t - J.tiles[b];
-        const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = J.k0 + (lt % J.ntk) * FK;
+        const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = (lt % J.ntk) * FK;
+        // a box row must start 16-byte aligned (an odd start coordinate, or a
+        // negative one, is an illegal instruction): from kb - 2, or 0
+        const int kbox = kb > 0 ? kb - 2 : 0;
         hx::mbar_expect_tx(&bar[s], FACE_BYTES);
         if (J.axis[b] == 0)
-            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapx, kb - 1, r0 - 1, J.pos[b] - 1, &bar[s]);
+            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapx, kbox, r0 - 1, J.pos[b] - 1, &bar[s]);
         else
-            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapy, kb - 1, J.pos[b] - 1, r0 - 1, &bar[s]);
+            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapy, kbox, J.pos[b] - 1, r0 - 1, &bar[s]);
     };
     if (threadIdx.x == 0) {
         base = step ? *(volatile unsigned long long *)step : 0ull;
@@ -692,7 +697,9 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         int b = 0;
         while (t >= J.tiles[b + 1]) ++b;
         const int lt = t - J.tiles[b];
-        const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = J.k0 + (lt % J.ntk) * FK;
+        // tiles start at even k, so every row segment [kb, kb + FK) starts on a
+        // 16-byte boundary here and on the neighbour (even row pitch)
+        const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = (lt % J.ntk) * FK;
         const bool xs = J.axis[b] == 0;
         const int row = r0 + w;
         const int i = xs ? J.pos[b] : row, j = xs ? row : J.pos[b];
@@ -710,8 +717,11 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
             }
         // shared-memory strides: x slab S[3][FBR][FBK], y slab S[FBR][3][FBK]
         const int ssx = xs ? FBR * FBK : 3 * FBK;
-        const int C0 = (xs ? (FBR + w + 1) : (3 * (w + 1) + 1)) * FBK + 1 + lane;
-        const int nk = row < J.hi[b] ? min(FK, J.k1 - kb) : 0;  // live columns of this row
+        // cell kk of the row sits at box column kk + 2 (box from kb - 2), or
+        // kk for the first tile (box from 0: its cell k = 0 is not relaxed)
+        const int C0 = (xs ? (FBR + w + 1) : (3 * (w + 1) + 1)) * FBK + (kb > 0 ? 2 : 0) + lane;
+        // live columns kk in [klo, khi): interior cells k in [k0, k1) of this row
+        const int klo = max(0, J.k0 - kb), khi = row < J.hi[b] ? min(FK, J.k1 - kb) : 0;
         hx::mbar_wait(&bar[s], (n / FNST) & 1);
         const double *S = reinterpret_cast<const double *>(smem + s * FACE_STRIDE);
         constexpr int U = FK / 32;
@@ -733,20 +743,91 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         if (res) {
 #pragma unroll
             for (int u = 0; u < U; ++u)
-                if (lane + 32 * u < nk) worst = max(worst, abs_diff_bits(v[u], S[C0 + 32 * u]));
+                if (lane + 32 * u >= klo && lane + 32 * u < khi)
+                    worst = max(worst, abs_diff_bits(v[u], S[C0 + 32 * u]));
         }
-        // every shared load has completed once the barrier is passed: each
-        // value fed v, and the residual's centre loads feed the predicate
-        (void)__syncthreads_or(res ? (int)(worst >> 63) : (int)(v[0] != v[0]));
-        if (threadIdx.x == 0 && n + FNST < count) load(n + FNST, s);  // refill during the stores
+        // cells outside the interior keep their current value (the bulk
+        // segment's end cells; never stored locally)
+        int nanp = 0;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int kk = lane + 32 * u;
-            if (kk >= nk) continue;
+            if (kk < klo || kk >= khi) v[u] = S[C0 + 32 * u];
+            nanp |= v[u] != v[u];
+        }
+        // every shared load has completed once the barrier is passed: each
+        // value fed v, and v and the residual feed the predicate, so the
+        // stage may be refilled right after it
+        (void)__syncthreads_or(nanp | (res ? (int)(worst >> 63) : 0));
+        if (threadIdx.x == 0 && n + FNST < count) load(n + FNST, s);  // refill during the stores
+        if (bulk == 2 && khi > klo) {
+            // paired 16-byte stores: the row is staged in shared memory, then
+            // each lane stores two adjacent cells (512 B per warp instruction,
+            // 16-byte aligned here and on the neighbour)
+            double *row_out = outrow + w * FK;
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < U; ++u) row_out[lane + 32 * u] = v[u];
+            __syncwarp();
+#pragma unroll
+            for (int h = 0; h < FK / 64; ++h) {
+                const int kk = 2 * lane + 64 * h;
+                if (kb + kk >= (int)pz) continue;
+                const double2 pr = *reinterpret_cast<const double2 *>(row_out + kk);
+                if (rd0) *reinterpret_cast<double2 *>(rd0 + kk) = pr;
+                if (rd1) *reinterpret_cast<double2 *>(rd1 + kk) = pr;
+                const bool l0 = kk >= klo && kk < khi, l1 = kk + 1 >= klo && kk + 1 < khi;
+                if (l0 && l1)
+                    *reinterpret_cast<double2 *>(dst + kk) = pr;
+                else if (l0)
+                    dst[kk] = pr.x;
+                else if (l1)
+                    dst[kk + 1] = pr.y;
+            }
+            continue;
+        }
+        if (bulk == 1 && rd0 && khi > klo) {
+            // the neighbour's copy leaves as whole 16-byte-aligned row
+            // segments by bulk copy (full 128-byte lines over NVLink; a
+            // warp's plain 8-byte stores straddle line boundaries). The
+            // segment's end cells k = 0 / bz + 1 land on the neighbour's
+            // edge cells (ghost plane x z ghost), which no stencil reads.
+            double *row_out = outrow + w * FK;
+            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            __syncwarp();
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int kk = lane + 32 * u;
+                row_out[kk] = v[u];
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) {
+                const unsigned bytes = (unsigned)(min(FK, (int)pz - kb) * sizeof(double));
+                const uint32_t src = hx::smem_addr(row_out);
+                asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                             ::"l"(rd0), "r"(src), "r"(bytes) : "memory");
+                if (rd1)
+                    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                                 ::"l"(rd1), "r"(src), "r"(bytes) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+            }
+            rd0 = rd1 = nullptr;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int kk = lane + 32 * u;
+            if (kk < klo || kk >= khi) continue;
             dst[kk] = v[u];
             if (rd0) rd0[kk] = v[u];
             if (rd1) rd1[kk] = v[u];
         }
+    }
+    // every bulk store has completed (written, not only read out of shared
+    // memory) before this CTA's fence and arrival count
+    if (bulk == 1 && (threadIdx.x & 31) == 0) {
+        asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+        asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     if (res) warp_max_to_global(worst, res);
     __syncthreads();
@@ -1247,7 +1328,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         const int *x = J.box[q];
         const bool xslab = x[1] - x[0] == 1 && x[5] - x[4] > 1;
         const bool yslab = x[3] - x[2] == 1 && x[1] - x[0] > 1 && x[5] - x[4] > 1;
-        faces_only = (xslab || yslab) && x[4] == J.box[0][4] && x[5] == J.box[0][5];
+        faces_only = (xslab || yslab) && x[4] == 1 && x[5] == bz + 1;
     }
     if (faces_only) {
         FaceJob F;
@@ -1255,7 +1336,7 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         F.nbox = J.nbox;
         F.k0 = J.box[0][4];
         F.k1 = J.box[0][5];
-        F.ntk = (F.k1 - F.k0 + FK - 1) / FK;
+        F.ntk = (bz + 2 + FK - 1) / FK;  // tiles over padded k [0, bz + 2), starting at even k
         F.tiles[0] = 0;
         for (int q = 0; q < J.nbox; ++q) {
             const int *x = J.box[q];
@@ -1280,6 +1361,11 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         if (int rc = face_map_for(cur, bx, by, bz, FBK, 3, FBR, &my)) return rc;
         static unsigned long long attr_set = 0;
         if (int rc = ensure_smem(face_tma_kernel, FACE_SMEM, attr_set)) return rc;
+        static int face_bulk = -1;  // bulk-copy row segments to the peer (HX_FACE_BULK=0: plain stores)
+        if (face_bulk < 0) {
+            const char *e = getenv("HX_FACE_BULK");
+            face_bulk = e ? atoi(e) : 1;
+        }
         static int fmult = 0;
         if (!fmult) {
             const char *e = getenv("HX_FACE_GRID_MULT");  // persistent CTAs per SM (tuning)
@@ -1288,7 +1374,8 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         const unsigned grid = (unsigned)std::max(1, std::min(F.tiles[F.nbox], fmult * num_sms()));
         if (F.tiles[F.nbox] > 0) {
             face_tma_kernel<<<grid, 256, FACE_SMEM, (cudaStream_t)stream>>>(
-                mx, my, nxt, by, bz, F, wait_value, signal_value, counter, timeout_ns, err, res,
+                mx, my, nxt, by, bz, F, face_bulk, wait_value, signal_value, counter, timeout_ns,
+                err, res,
                 step);
             HX_LAUNCH_CHECK();
             return 0;
