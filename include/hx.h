@@ -187,6 +187,20 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
                  unsigned long long *const signal_flag[6], unsigned long long signal_value,
                  unsigned int *counter, unsigned long long timeout_ns, int *err,
                  unsigned long long *res, unsigned long long *step, void *stream);
+/* hx_shell_put with the z faces through contiguous slots: zin[0] / zin[1]
+ * hold the -z / +z neighbour's face of the previous step, packed [i-1][j-1]
+ * (bx x by doubles, the arena slots the prime exchange also fills); they
+ * replace the ghost column. zout[0] / zout[1] receive this step's -z / +z
+ * face in the neighbour's arena (its slot for the next step), replacing
+ * 8-byte NVLink stores into its ghost column, one per 12 KB row. Either
+ * pointer pair may be NULL (ghost columns, as hx_shell_put). */
+int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int nbox,
+                   const int *boxes, double *const remote[6],
+                   unsigned long long *const wait_flag[6], unsigned long long wait_value,
+                   unsigned long long *const signal_flag[6], unsigned long long signal_value,
+                   unsigned int *counter, unsigned long long timeout_ns, int *err,
+                   unsigned long long *res, unsigned long long *step,
+                   const double *const zin[2], double *const zout[2], void *stream);
 
 /* --------------------------------------------------- persistent channel --
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper

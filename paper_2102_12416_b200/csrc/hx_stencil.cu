@@ -461,6 +461,13 @@ struct ShellJob {
     int face[6];            // coordinate of our plane facing d (i/j/k by d/2)
     unsigned long long *wait[6];
     unsigned long long *signal[6];
+    // z faces through contiguous slots (hx_shell_put_z): zin[h] holds the
+    // -z (h = 0) / +z (h = 1) neighbour's face of the previous step, packed
+    // [i-1][j-1] (bx x by), read instead of the ghost column; zout[h]
+    // receives our face on that side in the neighbour's arena, instead of
+    // 8-byte stores into its ghost column 12 KB apart
+    const double *zin[2];
+    double *zout[2];
 };
 
 __global__ void __launch_bounds__(256)
@@ -517,8 +524,18 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
             // Coherent (not .nc) loads: ghost cells were stored by a peer
             // GPU while this kernel may already have been running; the flag
             // acquire above (observed through the barrier) orders the loads.
-            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy],
-                                       cur[c - 1], cur[c + 1]));
+            double zm, zp;
+            const int kc = along_k ? x[4] + t : x[4];
+            const int jc = along_k ? j : j + t;
+            if (J.zin[0] && kc == 1)
+                zm = J.zin[0][(size_t)(i - 1) * by + (jc - 1)];
+            else
+                zm = cur[c - 1];
+            if (J.zin[1] && kc == bz)
+                zp = J.zin[1][(size_t)(i - 1) * by + (jc - 1)];
+            else
+                zp = cur[c + 1];
+            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy], zm, zp));
             if (res) worst = max(worst, abs_diff_bits(v, cur[c]));
             return v;
         };
@@ -535,7 +552,14 @@ shell_put_kernel(const double *cur, double *__restrict__ nxt, int by, int bz,
             }
 #pragma unroll
             for (int d = 0; d < 6; ++d)
-                if ((on >> d) & 1u) J.remote[d][(long long)c + J.shift[d]] = v;
+                if ((on >> d) & 1u) {
+                    if (d >= 4 && J.zout[d - 4]) {
+                        const int jj = along_k ? j : j + t;
+                        J.zout[d - 4][(size_t)(i - 1) * by + (jj - 1)] = v;
+                    } else {
+                        J.remote[d][(long long)c + J.shift[d]] = v;
+                    }
+                }
         };
         if (along_k && whole) {
             // The row lies on a face: store it to the neighbour in 16-byte
@@ -1281,6 +1305,18 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
                  unsigned long long signal_value, unsigned int *counter,
                  unsigned long long timeout_ns, int *err, unsigned long long *res,
                  unsigned long long *step, void *stream) {
+    return hx_shell_put_z(cur, nxt, bx, by, bz, nbox, boxes, remote, wait_flag, wait_value,
+                          signal_flag, signal_value, counter, timeout_ns, err, res, step, nullptr,
+                          nullptr, stream);
+}
+
+int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int nbox,
+                   const int *boxes, double *const remote[6], unsigned long long *const wait_flag[6],
+                   unsigned long long wait_value, unsigned long long *const signal_flag[6],
+                   unsigned long long signal_value, unsigned int *counter,
+                   unsigned long long timeout_ns, int *err, unsigned long long *res,
+                   unsigned long long *step, const double *const zin[2], double *const zout[2],
+                   void *stream) {
     if (!cur || !nxt || !counter || bx < 1 || by < 1 || bz < 1 || nbox < 0 || nbox > 6)
         return HX_E_INVALID;
     if (nbox > 0 && !boxes) return HX_E_INVALID;
@@ -1297,6 +1333,11 @@ int hx_shell_put(const double *cur, double *nxt, int bx, int by, int bz, int nbo
         // plane ext (d odd) its ghost plane 0
         J.face[d] = (d & 1) ? ext[d >> 1] : 1;
         J.shift[d] = (d & 1) ? -span[d >> 1] : span[d >> 1];
+    }
+    for (int h = 0; h < 2; ++h) {
+        // a z slot only together with that z neighbour
+        J.zin[h] = (zin && J.remote[4 + h]) ? zin[h] : nullptr;
+        J.zout[h] = (zout && J.remote[4 + h]) ? zout[h] : nullptr;
     }
     J.rows[0] = 0;
     long long n = 0;

@@ -189,6 +189,7 @@ class HaloJacobi:
     """
 
     e2e_ring_slots = 4096  # device residual slots of step_e2e (zeroed when the ring wraps)
+    z_slots = True  # fused exchange: z faces through the contiguous arena slots (False: ghost columns)
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
                  policy: str = "reference", timeout_s: float = 30.0, overlap: bool = False,
@@ -566,11 +567,13 @@ class HaloJacobi:
             wait = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
             signal = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
             base = 0 if dev_step else it
+            zin, zout = self._zslots(b, it)
             mark.begin("exchange", b, c)
-            _lib.call("hx_shell_put", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
+            _lib.call("hx_shell_put_z", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz,
                       len(shells), flat, _lib.ptr_array(remote), _lib.ptr_array(wait), base + 1,
                       _lib.ptr_array(signal), base + 2, b.counters_ptr + 4, self.timeout_ns,
-                      b.err_ptr, rps[b.rank], b.step_ptr if dev_step else None, c.cuda_stream)
+                      b.err_ptr, rps[b.rank], b.step_ptr if dev_step else None, zin, zout,
+                      c.cuda_stream)
             mark.end("exchange", b, c)
             ev = torch.cuda.Event()
             ev.record(c)
@@ -602,6 +605,22 @@ class HaloJacobi:
             b.cur ^= 1
         self.it += 1
 
+    def _zslots(self, b: HaloBlock, it: int):
+        """z faces of the fused exchange travel through the arena slots
+        (packed [i][j], contiguous) instead of the ghost columns: step it
+        reads slot[it & 1] on each z side (filled by the neighbour's step
+        it - 1, or by the priming exchange for it = 0) and writes the
+        neighbour's slot[(it + 1) & 1]. The flag protocol is unchanged: the
+        neighbour's flag >= it + 1 also says it finished reading the slot
+        of that parity (its step it - 1)."""
+        zin = (_lib.ctypes.c_void_p * 2)()
+        zout = (_lib.ctypes.c_void_p * 2)()
+        for h, d in enumerate((4, 5)):
+            if d in b.nbr_dirs and self.z_slots:
+                zin[h] = b.slot_ptr(it & 1, d)
+                zout[h] = b.put_slot(d, (it + 1) & 1)
+        return zin, zout
+
     def time_shell_alone(self, reps: int = 5) -> float | None:
         """Median ms of one block's hx_shell_put with nothing else running
         and no flag waits or releases: the fused exchange's own speed (its
@@ -617,17 +636,19 @@ class HaloJacobi:
         flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
         nxt = b.cur ^ 1
         remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
+        zin, zout = self._zslots(b, self.it)
         args = (b.field_ptr(), b.field_ptr(nxt), b.bx, b.by, b.bz, len(shells), flat,
                 _lib.ptr_array(remote), _lib.ptr_array([None] * 6), 0, _lib.ptr_array([None] * 6),
-                0, b.counters_ptr + 4, self.timeout_ns, b.err_ptr, None, None, c.cuda_stream)
-        _lib.call("hx_shell_put", *args)  # warm (tensor maps, attributes)
+                0, b.counters_ptr + 4, self.timeout_ns, b.err_ptr, None, None, zin, zout,
+                c.cuda_stream)
+        _lib.call("hx_shell_put_z", *args)  # warm (tensor maps, attributes)
         times = []
         back_to_back = 8  # launches per timing: the host's submit cost stays off the clock
         for _ in range(reps):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(c)
             for _ in range(back_to_back):
-                _lib.call("hx_shell_put", *args)
+                _lib.call("hx_shell_put_z", *args)
             e1.record(c)
             c.synchronize()
             times.append(e0.elapsed_time(e1) / back_to_back)
