@@ -651,23 +651,36 @@ constexpr unsigned FACE_STRIDE = (FACE_BYTES + 127u) / 128u * 128u;
 constexpr unsigned FACE_STAGE_OUT = 8u * FK * sizeof(double);  // one result row per warp
 constexpr size_t FACE_SMEM = (size_t)FNST * FACE_STRIDE + FACE_STAGE_OUT + FNST * sizeof(uint64_t);
 
+// z face tiles: 8 i-rows (one warp each) x 32 j (one lane each) at k = pos;
+// the box holds k-cells kstart .. kstart+3 (16-byte aligned start) of 10 x 34
+// (i, j) rows
+constexpr int ZTJ = 32;
+constexpr int ZBK = 4, ZBJ = ZTJ + 2, ZBI = FR + 2;
+constexpr unsigned ZFACE_BYTES = (unsigned)(ZBK * ZBJ * ZBI * sizeof(double));
+
 struct FaceJob {
     int nbox;
-    int axis[4];   // 0: x slab (plane i = pos), 1: y slab (row j = pos)
-    int pos[4];
-    int lo[4], hi[4];  // rows across the face: j (x slab) or i (y slab), 1-based, half-open
+    int axis[6];   // 0: x slab (plane i = pos), 1: y slab (row j = pos), 2: z slab (k = pos)
+    int pos[6];
+    int lo[6], hi[6];    // rows: j (x slab) or i (y and z slabs), 1-based, half-open
+    int clo[6], chi[6];  // z slab: the j range
     int k0, k1;
-    int tiles[5];  // prefix tile counts
+    int tiles[7];  // prefix tile counts
     int ntk;
     double *remote[6];
     long long shift[6];
     int face[6];
     unsigned long long *wait[6];
     unsigned long long *signal[6];
+    // z neighbours' faces through the arena slots (packed [i-1][j-1], bx x by):
+    // zin[h] read instead of the z ghost column, zout[h] written for them
+    const double *zin[2];
+    double *zout[2];
 };
 
 __global__ void __launch_bounds__(256)
 face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant__ CUtensorMap mapy,
+                const __grid_constant__ CUtensorMap mapz,
                 double *__restrict__ nxt, int by, int bz, FaceJob J, int bulk,
                 unsigned long long wait_value, unsigned long long signal_value, unsigned *counter,
                 unsigned long long timeout_ns, int *err, unsigned long long *res,
@@ -685,6 +698,14 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         int b = 0;
         while (t >= J.tiles[b + 1]) ++b;
         const int lt = t - J.tiles[b];
+        if (J.axis[b] == 2) {  // z face tile
+            const int ntj = (J.chi[b] - J.clo[b] + ZTJ - 1) / ZTJ;
+            const int i0 = J.lo[b] + (lt / ntj) * FR, j0 = J.clo[b] + (lt % ntj) * ZTJ;
+            const int kstart = J.pos[b] == 1 ? 0 : J.pos[b] - 2;
+            hx::mbar_expect_tx(&bar[s], ZFACE_BYTES);
+            hx::tma_load_3d(smem + s * FACE_STRIDE, &mapz, kstart, j0 - 1, i0 - 1, &bar[s]);
+            return;
+        }
         const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = (lt % J.ntk) * FK;
         // a box row must start 16-byte aligned (an odd start coordinate, or a
         // negative one, is an illegal instruction): from kb - 2, or 0
@@ -706,6 +727,7 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         if (ok && count) {
             hx::prefetch_tmap(&mapx);
             hx::prefetch_tmap(&mapy);
+            hx::prefetch_tmap(&mapz);
             for (int s = 0; s < FNST; ++s) hx::mbar_init(&bar[s], 1);
             hx::fence_mbar_init();
             for (int n = 0; n < FNST && n < count; ++n) load(n, n);
@@ -721,6 +743,31 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         int b = 0;
         while (t >= J.tiles[b + 1]) ++b;
         const int lt = t - J.tiles[b];
+        if (J.axis[b] == 2) {
+            // z face tile: cell (i0 + w, j0 + lane, pos). The neighbour-side
+            // z value comes from its slot (packed, coalesced along j); the
+            // result goes to nxt (one cell per 12 KB row) and to the
+            // neighbour's slot (contiguous).
+            const int ntj = (J.chi[b] - J.clo[b] + ZTJ - 1) / ZTJ;
+            const int i = J.lo[b] + (lt / ntj) * FR + w, j = J.clo[b] + (lt % ntj) * ZTJ + lane;
+            const int kf = J.pos[b], h = kf == 1 ? 0 : 1;
+            const bool live = i < J.hi[b] && j < J.chi[b];
+            const size_t packed = (size_t)(i - 1) * by + (j - 1);
+            const double ghost = live ? J.zin[h][packed] : 0.0;
+            const int C = ((w + 1) * ZBJ + lane + 1) * ZBK + (kf == 1 ? 1 : 2);
+            hx::mbar_wait(&bar[s], (n / FNST) & 1);
+            const double *S = reinterpret_cast<const double *>(smem + s * FACE_STRIDE);
+            const double zm = h == 0 ? ghost : S[C - 1], zp = h == 1 ? ghost : S[C + 1];
+            double v = div6(sum6(S[C - ZBJ * ZBK], S[C + ZBJ * ZBK], S[C - ZBK], S[C + ZBK], zm, zp));
+            if (res && live) worst = max(worst, abs_diff_bits(v, S[C]));
+            (void)__syncthreads_or((int)(v != v) | (res ? (int)(worst >> 63) : 0));
+            if (threadIdx.x == 0 && n + FNST < count) load(n + FNST, s);
+            if (live) {
+                nxt[((size_t)i * (by + 2) + j) * pz + kf] = v;
+                J.zout[h][packed] = v;
+            }
+            continue;
+        }
         // tiles start at even k, so every row segment [kb, kb + FK) starts on a
         // 16-byte boundary here and on the neighbour (even row pitch)
         const int r0 = J.lo[b] + (lt / J.ntk) * FR, kb = (lt % J.ntk) * FK;
@@ -748,6 +795,18 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         const int klo = max(0, J.k0 - kb), khi = row < J.hi[b] ? min(FK, J.k1 - kb) : 0;
         hx::mbar_wait(&bar[s], (n / FNST) & 1);
         const double *S = reinterpret_cast<const double *>(smem + s * FACE_STRIDE);
+        const int kbox = kb > 0 ? kb - 2 : 0;
+        if ((J.zin[0] || J.zin[1]) && row < J.hi[b]) {
+            // this row's z ghosts (k = 0, k = bz + 1) come from the z
+            // neighbours' slots, not the ghost column; only this warp reads them
+            double *Sw = reinterpret_cast<double *>(smem + s * FACE_STRIDE);
+            const int rs = C0 - lane - (kb > 0 ? 2 : 0) - kbox;  // (virtual) index of k = 0
+            const size_t packed = (size_t)(i - 1) * by + (j - 1);
+            if (lane == 0 && J.zin[0] && kb == 0) Sw[rs] = J.zin[0][packed];
+            if (lane == 0 && J.zin[1] && kb <= bz && bz < kb + FK) Sw[rs + bz + 1] = J.zin[1][packed];
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // before any TMA refill
+            __syncwarp();
+        }
         constexpr int U = FK / 32;
         double v[U];
         bool fast = true;
@@ -784,6 +843,16 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
         // stage may be refilled right after it
         (void)__syncthreads_or(nanp | (res ? (int)(worst >> 63) : 0));
         if (threadIdx.x == 0 && n + FNST < count) load(n + FNST, s);  // refill during the stores
+        if ((J.zout[0] || J.zout[1]) && khi > klo) {  // the row's z-face cells, for the z neighbours
+            const size_t packed = (size_t)(i - 1) * by + (j - 1);
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int kk = lane + 32 * u;
+                if (kk < klo || kk >= khi) continue;
+                if (J.zout[0] && kb + kk == 1) J.zout[0][packed] = v[u];
+                if (J.zout[1] && kb + kk == bz) J.zout[1][packed] = v[u];
+            }
+        }
         if (bulk == 2 && khi > klo) {
             // paired 16-byte stores: the row is staged in shared memory, then
             // each lane stores two adjacent cells (512 B per warp instruction,
@@ -1362,14 +1431,18 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
         const char *e = getenv("HX_SHELL_FACE_TMA");
         face_tma = e ? atoi(e) : 1;
     }
-    bool faces_only = face_tma && J.nbox > 0 && J.nbox <= 4 && tma_eligible(cur, bz) &&
-                      ((uintptr_t)nxt & 15) == 0 && !J.remote[4] && !J.remote[5] &&
-                      bx >= 2 && by >= 2;  // a row then lies on at most two neighbour faces
+    // x / y slabs over whole rows and z slabs at k = 1 / bz; z neighbours only
+    // through their slots; a row then lies on at most two x / y faces
+    bool faces_only = face_tma && J.nbox > 0 && tma_eligible(cur, bz) &&
+                      ((uintptr_t)nxt & 15) == 0 && (!J.remote[4] || J.zin[0]) &&
+                      (!J.remote[5] || J.zin[1]) && bx >= 2 && by >= 2 && bz >= 2;
     for (int q = 0; q < J.nbox && faces_only; ++q) {
         const int *x = J.box[q];
-        const bool xslab = x[1] - x[0] == 1 && x[5] - x[4] > 1;
-        const bool yslab = x[3] - x[2] == 1 && x[1] - x[0] > 1 && x[5] - x[4] > 1;
-        faces_only = (xslab || yslab) && x[4] == 1 && x[5] == bz + 1;
+        const bool xslab = x[1] - x[0] == 1 && x[4] == 1 && x[5] == bz + 1;
+        const bool yslab = x[3] - x[2] == 1 && x[1] - x[0] > 1 && x[4] == 1 && x[5] == bz + 1;
+        const bool zslab = x[5] - x[4] == 1 && (x[4] == 1 || x[4] == bz) && x[1] - x[0] >= 1 &&
+                           x[3] - x[2] > 1;
+        faces_only = xslab || yslab || zslab;
     }
     if (faces_only) {
         FaceJob F;
@@ -1381,14 +1454,29 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
         F.tiles[0] = 0;
         for (int q = 0; q < J.nbox; ++q) {
             const int *x = J.box[q];
-            const bool xslab = x[1] - x[0] == 1;
-            F.axis[q] = xslab ? 0 : 1;
-            F.pos[q] = xslab ? x[0] : x[2];
-            F.lo[q] = xslab ? x[2] : x[0];
-            F.hi[q] = xslab ? x[3] : x[1];
-            const long long t = (long long)((F.hi[q] - F.lo[q] + FR - 1) / FR) * F.ntk;
+            long long t;
+            if (x[5] - x[4] == 1) {  // z slab
+                F.axis[q] = 2;
+                F.pos[q] = x[4];
+                F.lo[q] = x[0];
+                F.hi[q] = x[1];
+                F.clo[q] = x[2];
+                F.chi[q] = x[3];
+                t = (long long)((x[1] - x[0] + FR - 1) / FR) * ((x[3] - x[2] + ZTJ - 1) / ZTJ);
+            } else {
+                const bool xslab = x[1] - x[0] == 1;
+                F.axis[q] = xslab ? 0 : 1;
+                F.pos[q] = xslab ? x[0] : x[2];
+                F.lo[q] = xslab ? x[2] : x[0];
+                F.hi[q] = xslab ? x[3] : x[1];
+                t = (long long)((F.hi[q] - F.lo[q] + FR - 1) / FR) * F.ntk;
+            }
             if (F.tiles[q] + t > 0x7fffffffLL) return HX_E_INVALID;
             F.tiles[q + 1] = F.tiles[q] + (int)t;
+        }
+        for (int h = 0; h < 2; ++h) {
+            F.zin[h] = J.zin[h];
+            F.zout[h] = J.zout[h];
         }
         for (int d = 0; d < 6; ++d) {
             F.remote[d] = J.remote[d];
@@ -1397,9 +1485,10 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
             F.wait[d] = J.wait[d];
             F.signal[d] = J.signal[d];
         }
-        CUtensorMap mx, my;
+        CUtensorMap mx, my, mz;
         if (int rc = face_map_for(cur, bx, by, bz, FBK, FBR, 3, &mx)) return rc;
         if (int rc = face_map_for(cur, bx, by, bz, FBK, 3, FBR, &my)) return rc;
+        if (int rc = face_map_for(cur, bx, by, bz, ZBK, ZBJ, ZBI, &mz)) return rc;
         static unsigned long long attr_set = 0;
         if (int rc = ensure_smem(face_tma_kernel, FACE_SMEM, attr_set)) return rc;
         static int face_bulk = -1;  // bulk-copy row segments to the peer (HX_FACE_BULK=0: plain stores)
@@ -1415,7 +1504,7 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
         const unsigned grid = (unsigned)std::max(1, std::min(F.tiles[F.nbox], fmult * num_sms()));
         if (F.tiles[F.nbox] > 0) {
             face_tma_kernel<<<grid, 256, FACE_SMEM, (cudaStream_t)stream>>>(
-                mx, my, nxt, by, bz, F, face_bulk, wait_value, signal_value, counter, timeout_ns,
+                mx, my, mz, nxt, by, bz, F, face_bulk, wait_value, signal_value, counter, timeout_ns,
                 err, res,
                 step);
             HX_LAUNCH_CHECK();

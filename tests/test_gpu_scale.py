@@ -147,7 +147,8 @@ def test_bench_config_random_field_bitexact_vs_c_oracle(oracle_c, n):
 @pytest.mark.parametrize("dims,pes,grid", [
     ((1536, 768, 768), 2, (2, 1, 1)),     # configs[4] at N = 2
     ((1536, 1536, 768), 4, (2, 2, 1)),    # configs[4] at N = 4
-    ((768, 768, 1536), 2, (1, 1, 2)),     # a z split: strided faces at scale
+    ((768, 768, 1536), 2, (1, 1, 2)),     # a z split: z faces through the arena slots
+    ((1536, 1536, 1536), 8, (2, 2, 2)),   # the paper's (2,2,2) layout: every face, edge, corner
 ])
 def test_fused_exchange_at_scale_random_field_vs_c_oracle(oracle_c, dims, pes, grid):
     """The default multi-GPU exchange (hx_shell_put: boundary relax + peer
