@@ -202,6 +202,22 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
                    unsigned long long *res, unsigned long long *step,
                    const double *const zin[2], double *const zout[2], void *stream);
 
+/* Small blocks: `iters` fused iterations of one block in ONE launch
+ * (persistent CTAs, grid barriers between iterations). Per iteration: wait
+ * for every non-NULL wait_flag[d] >= it + 1, relax the whole block
+ * field[parity] -> field[parity ^ 1], store each neighbour-facing cell also
+ * into peer[2 d + (parity ^ 1)] (the neighbour's next buffer, same padded
+ * shape) at its ghost plane, then release signal_flag[d] = it + 2; parity
+ * flips every iteration, it = it0 .. it0 + iters - 1. The same flag protocol
+ * as hx_shell_put, so runs may alternate with fused steps. barrier: two
+ * zero-initialised uint32 (count, generation). max_ctas caps the grid (every
+ * CTA must be co-resident with the other blocks' kernels on this GPU). */
+int hx_persist_run(double *const field[2], double *const peer[12], int bx, int by, int bz,
+                   int parity, unsigned long long it0, int iters,
+                   unsigned long long *const wait_flag[6], unsigned long long *const signal_flag[6],
+                   unsigned *barrier, int max_ctas, unsigned long long timeout_ns, int *err,
+                   void *stream);
+
 /* --------------------------------------------------- persistent channel --
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper
  * §3.2.2) in its pre-registered device form. One direction is a ring of

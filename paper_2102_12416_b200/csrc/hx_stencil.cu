@@ -940,6 +940,87 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
     }
 }
 
+// ---------------------------------------------- persistent small blocks --
+// Small blocks are launch-bound: a 64^3 sweep is ~1 us of HBM work, while a
+// fused step costs two launches plus their gaps even when replayed from a
+// CUDA graph. persist_kernel runs `iters` fused iterations of ONE block in
+// one launch: every iteration waits for the neighbours' flags (their
+// boundary of it-1 is in our ghost planes, and they are done reading the
+// ghosts we are about to write), relaxes the whole block — storing each
+// neighbour-facing cell also into the neighbour's next-buffer ghost plane,
+// as hx_shell_put does — then a grid barrier, and one thread releases
+// flag = it + 2 to every neighbour. Grid-wide barriers need every CTA
+// resident: the host sizes the grid to fit (hx_persist_run).
+struct PersistJob {
+    double *field[2];        // our two padded fields
+    double *peer[6][2];      // each neighbour's two fields (null: no neighbour)
+    long long shift[6];      // our padded offset + shift[d] = its ghost cell
+    int face[6];
+    unsigned long long *wait[6];
+    unsigned long long *signal[6];
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned g = *(volatile unsigned *)gen;
+        __threadfence();
+        if (atomicAdd(count, 1u) + 1u == gridDim.x) {
+            *count = 0u;
+            __threadfence();
+            atomicAdd(gen, 1u);  // release the others
+        } else {
+            while (*(volatile unsigned *)gen == g) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(256)
+persist_kernel(PersistJob J, int bx, int by, int bz, int parity, unsigned long long it0, int iters,
+               unsigned *bar_count, unsigned *bar_gen, unsigned long long timeout_ns, int *err) {
+    __shared__ int ok;
+    const hx::Geom g(by, bz);
+    const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
+    const long long cells = (long long)bx * by * bz;
+    for (int n = 0; n < iters; ++n) {
+        const unsigned long long it = it0 + n;
+        const int p = (parity + n) & 1;
+        if (threadIdx.x == 0) {
+            ok = 1;
+            if (blockIdx.x == 0)
+                for (int d = 0; d < 6 && ok; ++d)
+                    if (J.wait[d]) ok = hx::spin_until(J.wait[d], it + 1, timeout_ns, err);
+        }
+        grid_barrier(bar_count, bar_gen);  // CTA 0's acquires -> every CTA
+        if (err && *(volatile int *)err) return;  // a timed-out wait: everyone stops
+        const double *cur = J.field[p];
+        double *nxt = J.field[p ^ 1];
+        for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < cells;
+             q += (long long)gridDim.x * blockDim.x) {
+            const int k = 1 + (int)(q % bz);
+            const long long r = q / bz;
+            const int j = 1 + (int)(r % by), i = 1 + (int)(r / by);
+            const size_t c = g.at(i, j, k);
+            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy],
+                                       cur[c - 1], cur[c + 1]));
+            nxt[c] = v;
+            const int at[3] = {i, j, k};
+#pragma unroll
+            for (int d = 0; d < 6; ++d)
+                if (J.peer[d][p ^ 1] && at[d >> 1] == J.face[d])
+                    J.peer[d][p ^ 1][(long long)c + J.shift[d]] = v;
+        }
+        grid_barrier(bar_count, bar_gen);  // every CTA's local + peer stores are done
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            __threadfence_system();
+            for (int d = 0; d < 6; ++d)
+                if (J.signal[d]) hx::st_release_sys(J.signal[d], it + 2);
+        }
+    }
+}
+
 __global__ void fill_kernel(double *p, size_t n, double v) {
     for (size_t q = blockIdx.x * (size_t)blockDim.x + threadIdx.x; q < n;
          q += (size_t)gridDim.x * blockDim.x)
@@ -1521,6 +1602,42 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
                                (long long)mult * num_sms()));
     shell_put_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
         cur, nxt, by, bz, J, wait_value, signal_value, counter, timeout_ns, err, res, step);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
+int hx_persist_run(double *const field[2], double *const peer[12], int bx, int by, int bz,
+                   int parity, unsigned long long it0, int iters,
+                   unsigned long long *const wait_flag[6], unsigned long long *const signal_flag[6],
+                   unsigned *barrier, int max_ctas, unsigned long long timeout_ns, int *err,
+                   void *stream) {
+    if (!field || !field[0] || !field[1] || !barrier || bx < 1 || by < 1 || bz < 1 ||
+        iters < 0 || (parity & ~1))
+        return HX_E_INVALID;
+    if (iters == 0) return 0;
+    PersistJob J;
+    memset(&J, 0, sizeof(J));
+    const long long sx = (long long)(by + 2) * (bz + 2), sy = bz + 2;
+    const long long span[3] = {sx * bx, sy * by, (long long)bz};
+    const int ext[3] = {bx, by, bz};
+    J.field[0] = field[0];
+    J.field[1] = field[1];
+    for (int d = 0; d < 6; ++d) {
+        J.peer[d][0] = peer ? peer[2 * d] : nullptr;
+        J.peer[d][1] = peer ? peer[2 * d + 1] : nullptr;
+        J.wait[d] = wait_flag ? wait_flag[d] : nullptr;
+        J.signal[d] = signal_flag ? signal_flag[d] : nullptr;
+        J.face[d] = (d & 1) ? ext[d >> 1] : 1;
+        J.shift[d] = (d & 1) ? -span[d >> 1] : span[d >> 1];
+    }
+    // every CTA must be resident for the grid barriers: one CTA of 256
+    // threads per SM at most (the caller may lower it for blocks sharing a GPU)
+    const long long cells = (long long)bx * by * bz;
+    long long want = (cells + 1023) / 1024;
+    int grid = (int)std::max<long long>(1, std::min<long long>(want, num_sms()));
+    if (max_ctas > 0) grid = std::min(grid, max_ctas);
+    persist_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(J, bx, by, bz, parity, it0, iters,
+                                                           barrier, barrier + 1, timeout_ns, err);
     HX_LAUNCH_CHECK();
     return 0;
 }

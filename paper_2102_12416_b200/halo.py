@@ -697,6 +697,57 @@ class HaloJacobi:
             graphs[d] = g
         return graphs
 
+    def run_persistent(self, iters: int) -> None:
+        """``iters`` fused iterations with ONE kernel launch per block
+        (hx_persist_run: persistent CTAs, a grid barrier between
+        iterations, the same neighbour flags as the fused steps). Meant for
+        small blocks, where a step is ~1 us of HBM work and launches and
+        their gaps dominate even in a graph replay. Blocks sharing a GPU run
+        concurrently on their own streams with the SMs split between them
+        (their kernels wait on each other's flags, so all must be resident).
+        Same bits as run(); no residual."""
+        if self.exchange != "fused":
+            raise ValueError("run_persistent needs exchange='fused'")
+        if iters <= 0:
+            return
+        if self.it == 0:  # the priming exchange and step 0 stay outside (as run_graph)
+            self.step()
+            iters -= 1
+            if iters == 0:
+                return
+        per_dev = {}
+        for b in self.blocks.values():
+            per_dev.setdefault(b.device, []).append(b)
+        st = getattr(self, "_persist", None)
+        if st is None:
+            st = self._persist = {}
+        for b in self.blocks.values():  # every run starts after the last step's work ...
+            if b.rank not in st:
+                st[b.rank] = (torch.cuda.Stream(device=b.device),
+                              torch.zeros(2, dtype=torch.int32, device=f"cuda:{b.device}"))
+            st[b.rank][0].wait_stream(self.stream_of(b))
+        for dev, blocks in per_dev.items():  # ... all are launched (they wait on each other) ...
+            sms = _lib.ctypes.c_int(0)
+            _lib.call("hx_set_device", dev)
+            _lib.call("hx_sm_count", dev, _lib.ctypes.byref(sms))
+            cap = max(1, sms.value // len(blocks))
+            for b in blocks:
+                s, bar = st[b.rank]
+                fields = (_lib.ctypes.c_void_p * 2)(*[f.data_ptr() for f in b.fields])
+                peer = (_lib.ctypes.c_void_p * 12)()
+                for d in b.nbr_dirs:
+                    peer[2 * d], peer[2 * d + 1] = b.peer_fields[d]
+                wait = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
+                signal = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+                _lib.call("hx_persist_run", fields, peer, b.bx, b.by, b.bz, b.cur, self.it, iters,
+                          _lib.ptr_array(wait), _lib.ptr_array(signal), bar.data_ptr(), cap,
+                          self.timeout_ns, b.err_ptr, s.cuda_stream)
+        for b in self.blocks.values():  # ... and later steps follow every run
+            self.stream_of(b).wait_stream(st[b.rank][0])
+        for b in self.blocks.values():
+            b.cur ^= iters & 1
+        self.it += iters
+
     def run(self, iters: int, residual: bool = False) -> None:
         for _ in range(iters):
             self.step(residual)

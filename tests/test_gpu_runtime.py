@@ -518,3 +518,22 @@ def test_halo_engine_one_cell_thick_blocks(pkg, dims, pes, policy, exchange, ove
     want, _ = jacobi_np.sequential(dims, 7)
     assert eng.assemble().tobytes() == want.tobytes()
     eng.close()
+
+
+@pytest.mark.parametrize("dims,pes", [((48, 32, 40), 2), ((32, 32, 32), 8), ((30, 28, 26), 4),
+                                      ((17, 19, 64), 2), ((64, 64, 64), 1)])
+def test_persistent_kernel_run_bitexact(pkg, dims, pes):
+    """HaloJacobi.run_persistent (one launch per block for many fused
+    iterations: grid barriers, neighbour flags, peer ghost stores) gives the
+    oracle's bits, alone and alternating with ordinary fused steps."""
+    from oracle import jacobi_np
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, exchange="fused")
+    eng.run_persistent(9)
+    eng.step()
+    eng.run_persistent(6)
+    eng.check_errors()
+    want, _ = jacobi_np.sequential(dims, 16)
+    assert eng.assemble().tobytes() == want.tobytes()
+    eng.close()
