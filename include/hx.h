@@ -208,15 +208,18 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
  * field[parity] -> field[parity ^ 1], store each neighbour-facing cell also
  * into peer[2 d + (parity ^ 1)] (the neighbour's next buffer, same padded
  * shape) at its ghost plane, then release signal_flag[d] = it + 2; parity
- * flips every iteration, it = it0 .. it0 + iters - 1. The same flag protocol
- * as hx_shell_put, so runs may alternate with fused steps. barrier: two
+ * flips every iteration, it = it0 .. it0 + iters - 1. z faces go through
+ * the arena slots as in hx_shell_put_z: for an iteration of parity q (it & 1),
+ * zin[2 q + h] is our slot read on side h (-z, +z) and zout[2 q + h] the
+ * neighbour's slot written (its parity q ^ 1 slot); NULL: ghost columns. The same
+ * flag protocol as hx_shell_put, so runs may alternate with fused steps. barrier: two
  * zero-initialised uint32 (count, generation). max_ctas caps the grid (every
  * CTA must be co-resident with the other blocks' kernels on this GPU). */
 int hx_persist_run(double *const field[2], double *const peer[12], int bx, int by, int bz,
                    int parity, unsigned long long it0, int iters,
                    unsigned long long *const wait_flag[6], unsigned long long *const signal_flag[6],
-                   unsigned *barrier, int max_ctas, unsigned long long timeout_ns, int *err,
-                   void *stream);
+                   const double *const zin[4], double *const zout[4], unsigned *barrier,
+                   int max_ctas, unsigned long long timeout_ns, int *err, void *stream);
 
 /* --------------------------------------------------- persistent channel --
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper

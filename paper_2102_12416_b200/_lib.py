@@ -110,7 +110,8 @@ _SIGS = {
     "hx_shell_put": ([_V, _V, _I, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64,
                       ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V, _V], _I),
     "hx_persist_run": ([ctypes.POINTER(_V), ctypes.POINTER(_V), _I, _I, _I, _I, _U64, _I,
-                        ctypes.POINTER(_V), ctypes.POINTER(_V), _V, _I, _U64, _V, _V], _I),
+                        ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V),
+                        ctypes.POINTER(_V), _V, _I, _U64, _V, _V], _I),
     "hx_shell_put_z": ([_V, _V, _I, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64,
                         ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V, ctypes.POINTER(_V),
                         ctypes.POINTER(_V), _V], _I),

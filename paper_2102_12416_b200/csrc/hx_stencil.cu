@@ -958,6 +958,11 @@ struct PersistJob {
     int face[6];
     unsigned long long *wait[6];
     unsigned long long *signal[6];
+    // z faces through the arena slots, as the fused steps (hx_shell_put_z):
+    // for an iteration of parity q, zin[q][h] is our slot on side h (parity
+    // q) and zout[q][h] the neighbour's slot it writes (parity q ^ 1)
+    const double *zin[2][2];
+    double *zout[2][2];
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
@@ -1003,14 +1008,22 @@ persist_kernel(PersistJob J, int bx, int by, int bz, int parity, unsigned long l
             const long long r = q / bz;
             const int j = 1 + (int)(r % by), i = 1 + (int)(r / by);
             const size_t c = g.at(i, j, k);
-            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy],
-                                       cur[c - 1], cur[c + 1]));
+            const int qi = (int)(it & 1);  // zin[qi]: this iteration's slots; zout[qi]: the
+                                           // neighbour's slots for the next one
+            const size_t packed = (size_t)(i - 1) * by + (j - 1);
+            const double zm = (k == 1 && J.zin[qi][0]) ? J.zin[qi][0][packed] : cur[c - 1];
+            const double zp = (k == bz && J.zin[qi][1]) ? J.zin[qi][1][packed] : cur[c + 1];
+            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy], zm, zp));
             nxt[c] = v;
             const int at[3] = {i, j, k};
 #pragma unroll
             for (int d = 0; d < 6; ++d)
-                if (J.peer[d][p ^ 1] && at[d >> 1] == J.face[d])
-                    J.peer[d][p ^ 1][(long long)c + J.shift[d]] = v;
+                if (J.peer[d][p ^ 1] && at[d >> 1] == J.face[d]) {
+                    if (d >= 4 && J.zout[qi][d - 4])
+                        J.zout[qi][d - 4][packed] = v;
+                    else
+                        J.peer[d][p ^ 1][(long long)c + J.shift[d]] = v;
+                }
         }
         grid_barrier(bar_count, bar_gen);  // every CTA's local + peer stores are done
         if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -1609,8 +1622,8 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
 int hx_persist_run(double *const field[2], double *const peer[12], int bx, int by, int bz,
                    int parity, unsigned long long it0, int iters,
                    unsigned long long *const wait_flag[6], unsigned long long *const signal_flag[6],
-                   unsigned *barrier, int max_ctas, unsigned long long timeout_ns, int *err,
-                   void *stream) {
+                   const double *const zin[4], double *const zout[4], unsigned *barrier,
+                   int max_ctas, unsigned long long timeout_ns, int *err, void *stream) {
     if (!field || !field[0] || !field[1] || !barrier || bx < 1 || by < 1 || bz < 1 ||
         iters < 0 || (parity & ~1))
         return HX_E_INVALID;
@@ -1630,6 +1643,11 @@ int hx_persist_run(double *const field[2], double *const peer[12], int bx, int b
         J.face[d] = (d & 1) ? ext[d >> 1] : 1;
         J.shift[d] = (d & 1) ? -span[d >> 1] : span[d >> 1];
     }
+    for (int q = 0; q < 2; ++q)
+        for (int h = 0; h < 2; ++h) {  // only with that z neighbour
+            J.zin[q][h] = (zin && J.peer[4 + h][0]) ? zin[2 * q + h] : nullptr;
+            J.zout[q][h] = (zout && J.peer[4 + h][0]) ? zout[2 * q + h] : nullptr;
+        }
     // every CTA must be resident for the grid barriers: one CTA of 256
     // threads per SM at most (the caller may lower it for blocks sharing a GPU)
     const long long cells = (long long)bx * by * bz;

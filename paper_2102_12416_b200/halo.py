@@ -739,9 +739,14 @@ class HaloJacobi:
                     peer[2 * d], peer[2 * d + 1] = b.peer_fields[d]
                 wait = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
                 signal = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+                zin = (_lib.ctypes.c_void_p * 4)()
+                zout = (_lib.ctypes.c_void_p * 4)()
+                for q in (0, 1):  # both slot parities (as _zslots, per iteration)
+                    a, z = self._zslots(b, q)
+                    zin[2 * q], zin[2 * q + 1], zout[2 * q], zout[2 * q + 1] = a[0], a[1], z[0], z[1]
                 _lib.call("hx_persist_run", fields, peer, b.bx, b.by, b.bz, b.cur, self.it, iters,
-                          _lib.ptr_array(wait), _lib.ptr_array(signal), bar.data_ptr(), cap,
-                          self.timeout_ns, b.err_ptr, s.cuda_stream)
+                          _lib.ptr_array(wait), _lib.ptr_array(signal), zin, zout, bar.data_ptr(),
+                          cap, self.timeout_ns, b.err_ptr, s.cuda_stream)
         for b in self.blocks.values():  # ... and later steps follow every run
             self.stream_of(b).wait_stream(st[b.rank][0])
         for b in self.blocks.values():

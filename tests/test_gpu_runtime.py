@@ -529,7 +529,7 @@ def test_persistent_kernel_run_bitexact(pkg, dims, pes):
     from oracle import jacobi_np
     from paper_2102_12416_b200.halo import HaloJacobi
 
-    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, exchange="fused")
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, exchange="fused", timeout_s=10)
     eng.run_persistent(9)
     eng.step()
     eng.run_persistent(6)
