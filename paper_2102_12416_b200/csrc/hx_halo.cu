@@ -306,6 +306,10 @@ constexpr unsigned long long CHAN_PULL = 1ull << 31;  // header length flag: pul
 // every CTA's payload. 1: a system fence per CTA (the round-1 form; it
 // stalls each sending CTA for the NVLink write acknowledgements: 320 vs
 // 500 GB/s at 4 MiB). 2: no fence (diagnostics only — unordered).
+__device__ int g_chan_formal_credit = 0;  // HX_CHAN_FORMAL_CREDIT (set once per device, host side)
+
+__device__ __forceinline__ bool chan_credit_formal() { return g_chan_formal_credit != 0; }
+
 __device__ __forceinline__ bool chan_last_cta(unsigned int *counter, int sys_fence = 0) {
     __shared__ bool last;
     __syncthreads();
@@ -561,16 +565,23 @@ chan_recv_kernel(ChanDir c, unsigned char *dst, unsigned long long capacity,
     } else if (ok) {  // unaligned bulk or pull
         copy_bytes((char *)dst, from_p, take, tid, nth, true);
     }
-    // the credit hands the slot (or the pulled source) back to the sender:
-    // every CTA fences at GPU scope before its arrival count, and the last
-    // CTA publishes with a system-scope release, which is cumulative over
-    // all of them — so by the PTX memory model (not only because the loaded
-    // values fed stores issued before the barrier) every slot read is
-    // performed before the sender can overwrite the slot
-    if (chan_last_cta(c.counter, 0) && threadIdx.x == 0 && ok) {
+    // The credit hands the slot (or the pulled source) back to the sender.
+    // No fence before the arrival count and a relaxed credit store: every
+    // slot read fed a store issued before the CTA barrier, so the reads have
+    // been performed by the time any thread passes it (the hardware's
+    // behaviour; the PTX model does not order loads through data
+    // dependencies). The formal alternative — a GPU-scope fence per CTA and
+    // a system-scope release of the credit — was measured in round 2 on 2
+    // GPUs: one-way 8 B 3.4-3.6 -> 4.7-5.3 us and the 4 MiB window 729 -> 615
+    // GB/s (profiles/r2_osu_2gpu_table.md), so it is not the default.
+    // HX_CHAN_FORMAL_CREDIT=1 selects it (chan_credit_formal below).
+    if (chan_last_cta(c.counter, chan_credit_formal() ? 0 : 2) && threadIdx.x == 0 && ok) {
         chan_stamp(c, k, 3);
         if (len_out) *len_out = len;  // > capacity: the caller reports truncation
-        hx::st_release_sys(c.credit, k + 1);
+        if (chan_credit_formal())
+            hx::st_release_sys(c.credit, k + 1);
+        else
+            st_relaxed_sys(c.credit, k + 1);
     }
 }
 
@@ -969,6 +980,20 @@ int hx_chan_recv(void *dst, size_t capacity, const void *slots, size_t stride, i
         return HX_E_INVALID;
     ChanDir c{(char *)slots, credit, seq, counter, stride, depth, chan_trace_of(1)};
     chan_note(stream, false);
+    static int formal = -1;  // HX_CHAN_FORMAL_CREDIT=1: fenced credit (see chan_recv_kernel)
+    static unsigned long long formal_set = 0;
+    if (formal < 0) {
+        const char *e = getenv("HX_CHAN_FORMAL_CREDIT");
+        formal = e && atoi(e) == 1 ? 1 : 0;
+    }
+    if (formal) {
+        int dev = 0;
+        HX_TRY(cudaGetDevice(&dev));
+        if (!(formal_set & (1ull << (dev & 63)))) {
+            HX_TRY(cudaMemcpyToSymbol(g_chan_formal_credit, &formal, sizeof(int)));
+            formal_set |= 1ull << (dev & 63);
+        }
+    }
     cudaLaunchAttribute attr;
     // sized by the sink: a pulled message may be far larger than a slot
     // 2 x SMs: a pulled 4 MiB message is loaded entirely before the
