@@ -191,8 +191,8 @@ __device__ __forceinline__ Item work_item(int j0, int k0, int i0, int i1, int nt
 template <bool RES, int BOX_Z>
 __global__ void __launch_bounds__(THREADS, MIN_CTAS)
 stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__ nxt, int by,
-                   int bz, int i0, int i1, int j0, int j1, int k0, int k1, int ntj, int ntk,
-                   int chunk, int nchunks, int grows, unsigned long long *res) {
+                   int bz, int i0, int i1, int j0, int j1, int k0, int k1, int klive, int ntj,
+                   int ntk, int chunk, int nchunks, int grows, unsigned long long *res) {
     constexpr unsigned STAGE_BYTES = BOX_Y * BOX_Z * sizeof(double);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
@@ -223,7 +223,7 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
 #pragma unroll
     for (int p = 0; p < PTS; ++p) {
         const int r = warp + (p >> 1) * NWARP, kk = lane + 32 * (p & 1);
-        if (jb + r < j1 && kb + kk < k1) live |= 1u << p;
+        if (jb + r < j1 && kb + kk < k1 && kb + kk >= klive) live |= 1u << p;
     }
 
     double xm[PTS], x0[PTS];
@@ -1155,12 +1155,12 @@ int ensure_smem(Kernel kernel, size_t bytes, unsigned long long &done) {
 
 template <bool RES, int BOX_Z>
 int launch_tma_t(const CUtensorMap &map, double *nxt, int by, int bz, int i0, int i1, int j0,
-                 int j1, int k0, int k1, int ntj, int ntk, int chunk, int nchunks, int grows, long items,
-                 unsigned long long *res, cudaStream_t st) {
+                 int j1, int k0, int k1, int klive, int ntj, int ntk, int chunk, int nchunks,
+                 int grows, long items, unsigned long long *res, cudaStream_t st) {
     static unsigned long long attr_set = 0;
     if (int rc = ensure_smem(stencil_tma_kernel<RES, BOX_Z>, SMEM_BYTES, attr_set)) return rc;
     stencil_tma_kernel<RES, BOX_Z><<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
-        map, nxt, by, bz, i0, i1, j0, j1, k0, k1, ntj, ntk, chunk, nchunks, grows, res);
+        map, nxt, by, bz, i0, i1, j0, j1, k0, k1, klive, ntj, ntk, chunk, nchunks, grows, res);
     HX_LAUNCH_CHECK();
     return 0;
 }
@@ -1199,23 +1199,35 @@ Schedule make_schedule(int i0, int i1, int j0, int j1, int k0, int k1) {
 
 int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
                int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
-    // every tile starts at kb = k0 + t*TZ (TZ even): one box width per launch
-    const bool shifted = ((k0 - 1) & 1) != 0;
+    // every tile starts at kb = kt + t*TZ (TZ even): one box width per launch. A
+    // box whose first column k0 is even (a sweep trimmed by a -z neighbour)
+    // uses the 68-wide box shifted to a 16-byte-aligned start; its stores then
+    // start on even k. HX_TMA_KEEP_GRID=1 keeps the full sweep's tile grid
+    // instead (66-wide box from k0 - 1, stores below k0 masked via klive):
+    // measured slower, 8.90 vs 8.77 ms for a 1536^3 block trimmed at k = 2
+    // (tools/prof_box.py) — the shifted tiles' stores are 16-byte aligned
+    static int keep_grid = -1;
+    if (keep_grid < 0) {
+        const char *e = getenv("HX_TMA_KEEP_GRID");
+        keep_grid = e ? atoi(e) : 0;
+    }
+    const int kt = (((k0 - 1) & 1) && keep_grid) ? k0 - 1 : k0;
+    const bool shifted = ((kt - 1) & 1) != 0;
     const int box_z = shifted ? TZ + 4 : TZ + 2;
     CUtensorMap map;
     int rc = tensor_map_for(cur, bx, by, bz, box_z, &map);
     if (rc) return rc;
-    const Schedule sc = make_schedule(i0, i1, j0, j1, k0, k1);
+    const Schedule sc = make_schedule(i0, i1, j0, j1, kt, k1);
     if (sc.items > 0x7fffffffL) return HX_E_INVALID;
     if (shifted)
-        return res ? launch_tma_t<true, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj,
+        return res ? launch_tma_t<true, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
                                                 sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
-                   : launch_tma_t<false, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj,
+                   : launch_tma_t<false, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
                                                  sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
-    return res ? launch_tma_t<true, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk,
-                                            sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
-               : launch_tma_t<false, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, k0, k1, sc.ntj, sc.ntk,
-                                             sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
+    return res ? launch_tma_t<true, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
+                                            sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
+               : launch_tma_t<false, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
+                                             sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
 }
 
 // The four (row parity, plane parity) class maps of stencil_pair_kernel.
