@@ -217,6 +217,16 @@ def reference_update_sample(block: int, steps: int, warmup: int, planes: int = 1
     ctx = mp.get_context("fork")
     cores = sorted(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else list(
         range(os.cpu_count() or 1))
+    # each process holds two slab fields plus numpy's temporaries (~7 field
+    # sizes); keep the sample within half of the available host memory
+    per_proc = 8 * (planes + 2) * (block + 2) ** 2 * 8
+    try:
+        import psutil
+
+        avail = psutil.virtual_memory().available
+        cores = cores[:max(1, min(len(cores), int(avail * 0.5) // per_proc))]
+    except Exception:
+        cores = cores[:32]
     procs, pipes = [], []
     for c in cores:
         a, b = ctx.Pipe()
