@@ -420,12 +420,14 @@ def main() -> int:
     t_ms = max_over_ranks(t_local)
     sweep_cells = b.cells  # cells the timed TMA launch relaxes
     if (eng.overlap or eng.exchange == "fused") and b.nbr_dirs:
-        inner = eng.boxes(b)[0]
+        inner = (eng.fused_boxes(b) if eng.exchange == "fused" else eng.boxes(b))[0]
         sweep_cells = (inner[1] - inner[0]) * (inner[3] - inner[2]) * (inner[5] - inner[4])
         sten_ms = mean_ms("interior")  # the TMA interior launch alone
         exposed_ms = max_over_ranks(mean_ms("exposed"))
         if eng.exchange == "fused":
-            launches_per_step = 2  # interior + hx_shell_put
+            # interior + boundary kernel; with z neighbours the interior is three
+            # launches (middle + two z-edge strips) and hx_zsignal follows
+            launches_per_step = 2 + (3 if eng.z_interior(b) else 0)
         else:
             launches_per_step = 1 + len(eng.boxes(b)[1]) + 1 + 2 * len(b.nbr_dirs)
     else:

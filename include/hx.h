@@ -221,6 +221,24 @@ int hx_persist_run(double *const field[2], double *const peer[12], int bx, int b
                    const double *const zin[4], double *const zout[4], unsigned *barrier,
                    int max_ctas, unsigned long long timeout_ns, int *err, void *stream);
 
+/* The fused exchange's interior sweep when the block has z neighbours: the
+ * box must span whole z rows (k0 = 1, k1 = bz + 1). Tiles holding k = 1
+ * (zflag[0], -z) or k = bz (zflag[1], +z) wait for that flag >= *zstep + 1,
+ * read the ghost column from zin[h] (packed [i-1][j-1], bx x by) and copy the
+ * face cells into zout[h] (the neighbour's slot for the next step); the rest
+ * is hx_stencil_box. The z faces then cost no extra HBM traffic (the sweep
+ * stages those rows anyway). Not TMA-eligible or another box: HX_E_INVALID. */
+int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1,
+                     int j0, int j1, int k0, int k1, unsigned long long *res,
+                     const unsigned long long *const zflag[2], const unsigned long long *zstep,
+                     const double *const zin[2], double *const zout[2],
+                     unsigned long long timeout_ns, int *err, void *stream);
+/* After a step's interior sweep and boundary kernel (stream-ordered behind
+ * both): release flag[h] = *step + 2 into the z neighbours' arenas (skipped
+ * if *err != 0), then *step += 1. */
+int hx_zsignal(unsigned long long *const flag[2], unsigned long long *step, const int *err,
+               void *stream);
+
 /* --------------------------------------------------- persistent channel --
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper
  * §3.2.2) in its pre-registered device form. One direction is a ring of

@@ -128,11 +128,15 @@ __device__ __forceinline__ void warp_max_to_global(unsigned long long worst,
 // are advanced. Stores the live cells of plane q and folds their residual.
 // ROWSTEP: staged distance between a thread's rows r and r + NWARP; ylo /
 // yhi: distance from a cell to its y-1 / y+1 neighbour in P0.
-template <bool RES, int ROWSTEP>
+// ZE: cells p in zmask0 / zmask1 are also copied to zdst0 / zdst1 (+ the
+// row offset): a z face produced by the interior sweep (ZEdge below).
+template <bool RES, int ROWSTEP, bool ZE = false>
 __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, int soff, int ylo,
                                             int yhi, double (&xm)[PTS], double (&x0)[PTS],
                                             double *out, int bz, unsigned live,
-                                            unsigned long long &worst) {
+                                            unsigned long long &worst, double *zdst0 = nullptr,
+                                            unsigned zmask0 = 0, double *zdst1 = nullptr,
+                                            unsigned zmask1 = 0, int zrow = 0) {
     double v[PTS];
     bool fast = true;
 #pragma unroll
@@ -156,6 +160,10 @@ __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, 
         if (live & (1u << p)) {
             out[(size_t)((p >> 1) * NWARP) * (bz + 2) + 32 * (p & 1)] = v[p];
             if (RES) worst = max(worst, abs_diff_bits(v[p], xm[p]));
+            if (ZE) {
+                if ((zmask0 >> p) & 1u) zdst0[(p >> 1) * NWARP * zrow] = v[p];
+                if ((zmask1 >> p) & 1u) zdst1[(p >> 1) * NWARP * zrow] = v[p];
+            }
         }
     }
 }
@@ -188,11 +196,27 @@ __device__ __forceinline__ Item work_item(int j0, int k0, int i0, int i1, int nt
 // ------------------------------------------------------- TMA pipeline ----
 // Work item = (tile j, tile k, x chunk). Box in interior coordinates:
 // [i0,i1) x [j0,j1) x [k0,k1).
-template <bool RES, int BOX_Z>
-__global__ void __launch_bounds__(THREADS, MIN_CTAS)
+// The fused exchange's z faces produced by the interior sweep (round 2):
+// the tiles that hold k = 1 (with a -z neighbour) or k = bz (+z) wait for
+// that neighbour's flag (>= *step + 1), take the ghost column from its slot
+// (packed [i-1][j-1], patched into the staged planes) and copy the face
+// cells into the neighbour's slot. The z ghosts cost no extra HBM traffic:
+// the sweep stages those rows anyway, where a separate z-face kernel reads
+// one 32-byte sector per cell from rows 12 KB apart.
+struct ZEdge {
+    const unsigned long long *flag[2];  // our flags from the -z / +z neighbour (null: none)
+    const unsigned long long *step;     // device step counter (hx_zsignal advances it)
+    const double *zin[2];               // this step's slots
+    double *zout[2];                    // the neighbours' slots for the next step
+    unsigned long long timeout_ns;
+    int *err;
+};
+
+template <bool RES, int BOX_Z, bool ZE>
+__global__ void __launch_bounds__(THREADS, ZE ? 2 : MIN_CTAS)  // ZE: the edge strips only
 stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__ nxt, int by,
                    int bz, int i0, int i1, int j0, int j1, int k0, int k1, int klive, int ntj,
-                   int ntk, int chunk, int nchunks, int grows, unsigned long long *res) {
+                   int ntk, int chunk, int nchunks, int grows, unsigned long long *res, ZEdge Z) {
     constexpr unsigned STAGE_BYTES = BOX_Y * BOX_Z * sizeof(double);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
@@ -201,7 +225,15 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     const int jb = it.jb, kb = it.kb, ib = it.ib, nplanes = it.nplanes;
     const int kshift = BOX_Z == TZ + 2 ? 0 : (kb - 1) & 1;  // 16-byte aligned TMA rows
     const int kload = kb - 1 - kshift;
+    // z-edge tile: holds k = 1 (-z neighbour) / k = bz (+z neighbour)
+    const bool zlo = ZE && Z.flag[0] && kb <= 1 && 1 < kb + TZ && k0 <= 1;
+    const bool zhi = ZE && Z.flag[1] && kb <= bz && bz < kb + TZ && bz < k1;
 
+    if (ZE && threadIdx.x == 0 && (zlo || zhi)) {
+        const unsigned long long want = *(volatile const unsigned long long *)Z.step + 1;
+        if (zlo) hx::spin_until(Z.flag[0], want, Z.timeout_ns, Z.err);
+        if (zhi) hx::spin_until(Z.flag[1], want, Z.timeout_ns, Z.err);
+    }
     if (threadIdx.x == 0) {
         hx::prefetch_tmap(&map);
         for (int s = 0; s < NSTAGE; ++s) hx::mbar_init(&bar[s], 1);
@@ -226,6 +258,35 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
         if (jb + r < j1 && kb + kk < k1 && kb + kk >= klive) live |= 1u << p;
     }
 
+    // ZE: warp 0 patches the staged plane's z ghost column(s) from the
+    // slots (rows jb .. jb + 31 of padded plane P, relaxed planes only). The
+    // slot values are loaded one plane ahead into registers (zfetch), so the
+    // load latency hides behind the previous plane's relax.
+    const bool zrow = ZE && (zlo || zhi) && warp == 0 && jb + lane <= by;
+    double zg0 = 0.0, zg1 = 0.0;
+    auto zfetch = [&](int P) {  // the slot values of padded plane P (registers)
+        if (!zrow) return;
+        const size_t at = (size_t)(P - 1) * by + (jb + lane - 1);
+        if (zlo) zg0 = Z.zin[0][at];
+        if (zhi) zg1 = Z.zin[1][at];
+    };
+    auto zpatch = [&](double *S) {  // the values fetched last into the staged plane
+        if (!zrow) return;
+        if (zlo) S[(1 + lane) * BOX_Z + (0 - kload)] = zg0;
+        if (zhi) S[(1 + lane) * BOX_Z + (bz + 1 - kload)] = zg1;
+    };
+    // ZE: the face cells' copies into the neighbours' slots
+    double *zdst0 = nullptr, *zdst1 = nullptr;
+    unsigned zmask0 = 0, zmask1 = 0;
+    if (ZE && zlo && lane == (1 - kb)) {  // k = 1 is column 0 of the tile: lane 0, first half
+        zdst0 = Z.zout[0] + (size_t)(ib - 1) * by + (jb + warp - 1);
+        zmask0 = 0x55u;
+    }
+    if (ZE && zhi && lane == ((bz - kb) & 31)) {
+        zdst1 = Z.zout[1] + (size_t)(ib - 1) * by + (jb + warp - 1);
+        zmask1 = ((bz - kb) >> 5) ? 0xAAu : 0x55u;
+    }
+
     double xm[PTS], x0[PTS];
     unsigned long long worst = 0;
     int nan_seen = 0;
@@ -234,6 +295,12 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
         const double *s1 = reinterpret_cast<const double *>(smem + STAGE_STRIDE);
         hx::mbar_wait(&bar[0], 0);
         hx::mbar_wait(&bar[1], 0);
+        if (ZE && (zlo || zhi) && warp == 0) {
+            zfetch(ib);
+            zpatch(reinterpret_cast<double *>(smem + STAGE_STRIDE));  // plane ib: stage 1
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (nplanes - 2 >= 2) zfetch(ib + 1);  // the next relaxed plane, ahead
+        }
 #pragma unroll
         for (int p = 0; p < PTS; ++p) {
             const int o = soff + (p >> 1) * NWARP * BOX_Z + 32 * (p & 1);
@@ -258,10 +325,22 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     for (int q = 1; q <= nplanes - 2; ++q) {
         const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;  // stage holding plane q+1
         hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
-        relax_plane<RES, NWARP * BOX_Z>(reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
-                                reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE), soff,
-                                BOX_Z, BOX_Z, xm, x0, out, bz, live, worst);
+        // plane q + 1's ghost column, for its own relax next iteration (the
+        // barrier below orders it; relax_plane(q) reads only its centres)
+        if (ZE && (zlo || zhi) && warp == 0 && q + 1 <= nplanes - 2) {
+            zpatch(reinterpret_cast<double *>(smem + s_n * STAGE_STRIDE));  // plane q + 1
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            if (q + 2 <= nplanes - 2) zfetch(ib - 1 + q + 2);
+        }
+        relax_plane<RES, NWARP * BOX_Z, ZE>(
+            reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
+            reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE), soff, BOX_Z, BOX_Z, xm,
+            x0, out, bz, live, worst, zdst0, zmask0, zdst1, zmask1, 1);
         out += plane;
+        if (ZE) {
+            if (zdst0) zdst0 += by;
+            if (zdst1) zdst1 += by;
+        }
         __syncthreads();  // all warps are done with stage s_c (plane q)
         if (threadIdx.x == 0) {
             const int p = q + NSTAGE;
@@ -1153,14 +1232,14 @@ int ensure_smem(Kernel kernel, size_t bytes, unsigned long long &done) {
     return 0;
 }
 
-template <bool RES, int BOX_Z>
+template <bool RES, int BOX_Z, bool ZE>
 int launch_tma_t(const CUtensorMap &map, double *nxt, int by, int bz, int i0, int i1, int j0,
                  int j1, int k0, int k1, int klive, int ntj, int ntk, int chunk, int nchunks,
-                 int grows, long items, unsigned long long *res, cudaStream_t st) {
+                 int grows, long items, unsigned long long *res, const ZEdge &Z, cudaStream_t st) {
     static unsigned long long attr_set = 0;
-    if (int rc = ensure_smem(stencil_tma_kernel<RES, BOX_Z>, SMEM_BYTES, attr_set)) return rc;
-    stencil_tma_kernel<RES, BOX_Z><<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
-        map, nxt, by, bz, i0, i1, j0, j1, k0, k1, klive, ntj, ntk, chunk, nchunks, grows, res);
+    if (int rc = ensure_smem(stencil_tma_kernel<RES, BOX_Z, ZE>, SMEM_BYTES, attr_set)) return rc;
+    stencil_tma_kernel<RES, BOX_Z, ZE><<<(unsigned)items, THREADS, SMEM_BYTES, st>>>(
+        map, nxt, by, bz, i0, i1, j0, j1, k0, k1, klive, ntj, ntk, chunk, nchunks, grows, res, Z);
     HX_LAUNCH_CHECK();
     return 0;
 }
@@ -1198,7 +1277,12 @@ Schedule make_schedule(int i0, int i1, int j0, int j1, int k0, int k1) {
 }
 
 int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1, int j0,
-               int j1, int k0, int k1, unsigned long long *res, cudaStream_t st) {
+               int j1, int k0, int k1, unsigned long long *res, cudaStream_t st,
+               const ZEdge *zedge = nullptr) {
+    ZEdge Z;
+    memset(&Z, 0, sizeof(Z));
+    if (zedge) Z = *zedge;
+    const bool ze = zedge && (Z.flag[0] || Z.flag[1]);
     // every tile starts at kb = kt + t*TZ (TZ even): one box width per launch. A
     // box whose first column k0 is even (a sweep trimmed by a -z neighbour)
     // uses the 68-wide box shifted to a 16-byte-aligned start; its stores then
@@ -1219,15 +1303,17 @@ int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, i
     if (rc) return rc;
     const Schedule sc = make_schedule(i0, i1, j0, j1, kt, k1);
     if (sc.items > 0x7fffffffL) return HX_E_INVALID;
+#define HX_TMA_LAUNCH(R, W, E)                                                             \
+    launch_tma_t<R, W, E>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj, sc.ntk, sc.chunk, \
+                          sc.nchunks, sc.grows, sc.items, res, Z, st)
+    if (ze) {  // the z-edge variant: only unshifted boxes starting at k = 1 reach it (halo.py)
+        if (shifted) return HX_E_INVALID;
+        return res ? HX_TMA_LAUNCH(true, TZ + 2, true) : HX_TMA_LAUNCH(false, TZ + 2, true);
+    }
     if (shifted)
-        return res ? launch_tma_t<true, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
-                                                sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
-                   : launch_tma_t<false, TZ + 4>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
-                                                 sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
-    return res ? launch_tma_t<true, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
-                                            sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st)
-               : launch_tma_t<false, TZ + 2>(map, nxt, by, bz, i0, i1, j0, j1, kt, k1, k0, sc.ntj,
-                                             sc.ntk, sc.chunk, sc.nchunks, sc.grows, sc.items, res, st);
+        return res ? HX_TMA_LAUNCH(true, TZ + 4, false) : HX_TMA_LAUNCH(false, TZ + 4, false);
+    return res ? HX_TMA_LAUNCH(true, TZ + 2, false) : HX_TMA_LAUNCH(false, TZ + 2, false);
+#undef HX_TMA_LAUNCH
 }
 
 // The four (row parity, plane parity) class maps of stencil_pair_kernel.
@@ -1461,6 +1547,78 @@ int hx_stencil_box(const double *cur, double *nxt, int bx, int by, int bz, int i
     return launch_generic(cur, nxt, by, bz, i0, i1, j0, j1, k0, k1, res, st);
 }
 
+// The interior sweep of the fused exchange with the z faces (see ZEdge).
+int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1,
+                     int j0, int j1, int k0, int k1, unsigned long long *res,
+                     const unsigned long long *const zflag[2], const unsigned long long *zstep,
+                     const double *const zin[2], double *const zout[2],
+                     unsigned long long timeout_ns, int *err, void *stream) {
+    if (!cur || !nxt || bx < 1 || by < 1 || bz < 1 || !zstep || !zflag) return HX_E_INVALID;
+    if (i0 < 1 || j0 < 1 || k0 != 1 || i1 > bx + 1 || j1 > by + 1 || k1 != bz + 1)
+        return HX_E_INVALID;  // whole rows in z: the box holds both z faces
+    if (i0 >= i1 || j0 >= j1) return 0;
+    if (!tma_eligible(cur, bz)) return HX_E_INVALID;
+    ZEdge Z;
+    memset(&Z, 0, sizeof(Z));
+    for (int h = 0; h < 2; ++h) {
+        Z.flag[h] = zflag[h];
+        if (zflag[h] && (!zin || !zout || !zin[h] || !zout[h])) return HX_E_INVALID;
+        Z.zin[h] = zflag[h] ? zin[h] : nullptr;
+        Z.zout[h] = zflag[h] ? zout[h] : nullptr;
+    }
+    Z.step = zstep;
+    Z.timeout_ns = timeout_ns;
+    Z.err = err;
+    g_last_variant = 1;
+    cudaStream_t st = (cudaStream_t)stream;
+    // Only the tile columns that hold k = 1 or k = bz take the z-edge kernel
+    // (more registers, a flag wait, slot patches): the middle columns are a
+    // plain interior sweep on the same tile grid, launched first.
+    const int klo_end = 1 + TZ;                       // the first tile column: [1, 1 + TZ)
+    const int khi_beg = 1 + ((bz - 1) / TZ) * TZ;     // the tile column holding k = bz
+    if (khi_beg <= klo_end) {  // one or two tile columns: everything is an edge
+        return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, bz + 1, res, st, &Z);
+    }
+    if (khi_beg > klo_end)
+        if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, klo_end, khi_beg, res, st))
+            return rc;
+    ZEdge lo = Z, hi = Z;
+    lo.flag[1] = nullptr;
+    hi.flag[0] = nullptr;
+    if (Z.flag[0]) {
+        if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, klo_end, res, st, &lo))
+            return rc;
+    } else if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, klo_end, res, st)) {
+        return rc;
+    }
+    if (Z.flag[1])
+        return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, khi_beg, bz + 1, res, st, &hi);
+    return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, khi_beg, bz + 1, res, st);
+}
+
+// After a fused step's interior and boundary kernels: release the z
+// neighbours' flags (= *step + 2, cumulative over both kernels' slot
+// writes, which precede this launch on the stream) and advance *step.
+__global__ void zsignal_kernel(unsigned long long *f0, unsigned long long *f1,
+                               unsigned long long *step, const int *err) {
+    const unsigned long long v = *(volatile unsigned long long *)step + 2;
+    __threadfence_system();
+    const bool healthy = !err || *(volatile const int *)err == 0;
+    if (healthy) {
+        if (f0) hx::st_release_sys(f0, v);
+        if (f1) hx::st_release_sys(f1, v);
+    }
+    *step = v - 1;
+}
+
+int hx_zsignal(unsigned long long *const flag[2], unsigned long long *step, const int *err,
+               void *stream) {
+    if (!flag || !step) return HX_E_INVALID;
+    zsignal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag[0], flag[1], step, err);
+    HX_LAUNCH_CHECK();
+    return 0;
+}
+
 int hx_preload_halo_kernels();  // hx_halo.cu
 
 // See hx_preload_halo_kernels: the exchange's spinning kernels, loaded up
@@ -1470,6 +1628,7 @@ int hx_preload() {
     cudaFuncAttributes a;
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)shell_put_kernel));
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)face_tma_kernel));
+    HX_TRY(cudaFuncGetAttributes(&a, (const void *)zsignal_kernel));
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)fill_kernel));
     return hx_preload_halo_kernels();
 }

@@ -92,6 +92,8 @@ class HaloBlock:
             self.fields = [torch.empty(shape, dtype=torch.float64, device=dev) for _ in range(2)]
             self.arena = torch.zeros(self.arena_bytes, dtype=torch.uint8, device=dev)
             self.step_dev = torch.zeros(1, dtype=torch.int64, device=dev)  # graph replays
+            # z faces from the interior sweep: its step counter (hx_zsignal advances it)
+            self.zstep_dev = torch.zeros(1, dtype=torch.int64, device=dev)
         # filled by HaloJacobi.connect(): (neighbour arena base, its side)
         self.put_dst = [None] * NDIRS
         self.put_flag = [None] * NDIRS
@@ -189,6 +191,13 @@ class HaloJacobi:
     """
 
     e2e_ring_slots = 4096  # device residual slots of step_e2e (zeroed when the ring wraps)
+    # fused, z neighbours: True = the interior sweep produces and consumes the
+    # z faces (hx_stencil_box_z: two z-edge strip launches + hx_zsignal);
+    # False = the boundary kernel's z tiles do (default: measured faster, 18.04
+    # vs 19.56 ms for two 1536^3 blocks with a z split on one GPU,
+    # tools/prof_zshell.py — the edge strips run at 2 CTAs/SM and pay a slot
+    # patch per plane, more than the z tiles' scattered sectors cost)
+    z_from_interior = False
     z_slots = True  # fused exchange: z faces through the contiguous arena slots (False: ghost columns)
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
@@ -246,8 +255,10 @@ class HaloJacobi:
                           int(b.coords[0] == 0), 1.0, 0.0, 0.0, s)
             with torch.cuda.stream(self.stream_of(b)):
                 b.arena[:_HDR].zero_()
+                b.zstep_dev.zero_()
             b.cur = 0
         self.it = 0
+        self._zstep_stale = False
         self.synchronize()
 
     def fill_random(self, seed: int = 0) -> None:
@@ -406,6 +417,24 @@ class HaloJacobi:
             shells.append((lo[0], hi[0], lo[1], hi[1], b.bz, b.bz + 1))
         return inner, [x for x in shells if x[0] < x[1] and x[2] < x[3] and x[4] < x[5]]
 
+    def z_interior(self, b: HaloBlock) -> bool:
+        """Fused exchange with z neighbours: the interior TMA sweep spans
+        whole z rows and produces / consumes the z faces itself
+        (hx_stencil_box_z), so no kernel touches the z columns separately.
+        Needs a TMA-describable block (even bz, 16-byte aligned field)."""
+        return (self.z_from_interior and self.z_slots and (4 in b.nbr_dirs or 5 in b.nbr_dirs)
+                and (b.bz + 2) % 2 == 0 and b.fields[0].data_ptr() % 16 == 0 and b.bz >= 2)
+
+    def fused_boxes(self, b: HaloBlock):
+        """(interior box, boundary slabs) of a fused step: boxes(), except
+        that with z_interior the interior keeps whole z rows and the z slabs
+        are dropped."""
+        inner, shells = self.boxes(b)
+        if not self.z_interior(b):
+            return inner, shells
+        inner = (inner[0], inner[1], inner[2], inner[3], 1, b.bz + 1)
+        return inner, [x for x in shells if x[5] - x[4] > 1]
+
     def _box(self, b: HaloBlock, box, res_ptr, stream) -> None:
         if box[0] < box[1] and box[2] < box[3] and box[4] < box[5]:
             _lib.call("hx_stencil_box", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz,
@@ -552,6 +581,11 @@ class HaloJacobi:
         # residual slots first: a new slot is zero-filled on the main stream
         # before `ready` is recorded, so the shell's atomics follow the fill
         rps = {b.rank: self._res_ptr(b, it, residual) for b in blocks}
+        if self._zstep_stale:  # a persistent run advanced the steps without hx_zsignal
+            for b in self.blocks.values():
+                with torch.cuda.stream(self.stream_of(b)):
+                    b.zstep_dev.fill_(it)
+            self._zstep_stale = False
         for b in blocks:
             if not b.nbr_dirs:
                 continue
@@ -560,12 +594,15 @@ class HaloJacobi:
             ready = torch.cuda.Event()
             ready.record(s)  # the previous interior (and shell) finished
             c.wait_event(ready)
-            _, shells = self.boxes(b)
+            _, shells = self.fused_boxes(b)
+            zint = self.z_interior(b)
             flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
             nxt = b.cur ^ 1  # every block flips in lock step: the peer's nxt too
             remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
             wait = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
-            signal = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+            # with z_interior the z flags are released after both kernels (hx_zsignal)
+            signal = [b.put_flag[d] if d in b.nbr_dirs and not (zint and d >= 4) else None
+                      for d in range(NDIRS)]
             base = 0 if dev_step else it
             zin, zout = self._zslots(b, it)
             mark.begin("exchange", b, c)
@@ -587,8 +624,16 @@ class HaloJacobi:
             rp = rps[b.rank]
             mark.begin("sweep", b, s)
             mark.begin("interior", b, s)
-            if b.nbr_dirs:
-                inner, _ = self.boxes(b)
+            if b.nbr_dirs and self.z_interior(b):
+                inner, _ = self.fused_boxes(b)
+                zin, zout = self._zslots(b, it)
+                zflag = (ctypes.c_void_p * 2)(*[b.flag_ptr(d) if d in b.nbr_dirs else None
+                                               for d in (4, 5)])
+                _lib.call("hx_stencil_box_z", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by,
+                          b.bz, *inner, rp, zflag, b.zstep_dev.data_ptr(), zin, zout,
+                          self.timeout_ns, b.err_ptr, s.cuda_stream)
+            elif b.nbr_dirs:
+                inner, _ = self.fused_boxes(b)
                 self._box(b, inner, rp, s)
             else:
                 _lib.call("hx_stencil", b.field_ptr(), b.field_ptr(b.cur ^ 1), b.bx, b.by, b.bz,
@@ -601,6 +646,10 @@ class HaloJacobi:
             if b.rank in shell_done:
                 s.wait_event(shell_done[b.rank])
             mark.end("exposed", b, s)
+            if b.nbr_dirs and self.z_interior(b):  # both kernels done: release the z flags
+                zsig = (ctypes.c_void_p * 2)(*[b.put_flag[d] if d in b.nbr_dirs else None
+                                              for d in (4, 5)])
+                _lib.call("hx_zsignal", zsig, b.zstep_dev.data_ptr(), b.err_ptr, s.cuda_stream)
             mark.end("sweep", b, s)
             b.cur ^= 1
         self.it += 1
@@ -632,7 +681,7 @@ class HaloJacobi:
         _lib.call("hx_set_device", b.device)
         c = self.comm[b.device]
         self.synchronize()
-        _, shells = self.boxes(b)
+        _, shells = self.fused_boxes(b)
         flat = (ctypes.c_int * (6 * len(shells)))(*[v for box in shells for v in box])
         nxt = b.cur ^ 1
         remote = [b.peer_fields[d][nxt] if d in b.nbr_dirs else None for d in range(NDIRS)]
@@ -669,13 +718,16 @@ class HaloJacobi:
         if self.it == 0:  # the priming exchange and step 0 stay outside the graph
             self.step()
             iters -= 1
+        # the device step counters first: a capture must not record these fills
+        for b in self.blocks.values():
+            with torch.cuda.stream(self.stream_of(b)):
+                b.step_dev.fill_(self.it)
+                b.zstep_dev.fill_(self.it)
+        self._zstep_stale = False
         parity = next(iter(self.blocks.values())).cur
         graphs = self._graphs.get(parity)
         if graphs is None:
             graphs = self._graphs[parity] = self._capture_pair()
-        for b in self.blocks.values():
-            with torch.cuda.stream(self.stream_of(b)):
-                b.step_dev.fill_(self.it)
         for _ in range(iters // 2):
             for d, g in graphs.items():
                 with torch.cuda.device(d), torch.cuda.stream(self.streams[d]):
@@ -752,6 +804,7 @@ class HaloJacobi:
         for b in self.blocks.values():
             b.cur ^= iters & 1
         self.it += iters
+        self._zstep_stale = True
 
     def run(self, iters: int, residual: bool = False) -> None:
         for _ in range(iters):

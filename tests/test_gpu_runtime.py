@@ -537,3 +537,28 @@ def test_persistent_kernel_run_bitexact(pkg, dims, pes):
     want, _ = jacobi_np.sequential(dims, 16)
     assert eng.assemble().tobytes() == want.tobytes()
     eng.close()
+
+
+@pytest.mark.parametrize("dims,pes", [((32, 40, 64), 2), ((48, 48, 48), 8), ((40, 32, 96), 4)])
+def test_fused_z_faces_from_the_interior_sweep_bitexact(pkg, dims, pes):
+    """The alternative z-face path (HaloJacobi.z_from_interior: hx_stencil_box_z
+    edge strips wait for the z flags, patch the ghost column from the slots
+    and write the neighbour's slot; hx_zsignal releases the z flags) gives the
+    oracle's bits, through eager steps, graph replays and persistent runs."""
+    from oracle import jacobi_np
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, exchange="fused", timeout_s=10,
+                     policy="reference")
+    eng.z_from_interior = True
+    assert any(eng.z_interior(b) for b in eng.blocks.values())
+    eng.run(3, residual=True)
+    eng.run_graph(4)
+    eng.run_persistent(3)
+    eng.run(2)
+    eng.check_errors()
+    want, wres = jacobi_np.sequential(dims, 12)
+    assert eng.assemble().tobytes() == want.tobytes()
+    got = [max(eng.residuals(r)[i] for r in eng.blocks) for i in range(3)]
+    assert got == wres[:3]
+    eng.close()

@@ -1,6 +1,7 @@
 """The fused exchange on a z split: one block's boundary kernel alone
-(flags pre-satisfied, back-to-back launches) with the z faces through the
-contiguous arena slots vs the ghost columns, and full fused steps.
+(flags pre-satisfied, back-to-back launches) and full fused steps, with the
+z faces produced by the interior sweep (default), by the boundary kernel
+through the contiguous slots, or through the ghost columns.
 
     python tools/prof_zshell.py [--n 1536] [--two-gpus]
 """
@@ -21,8 +22,11 @@ def main():
     eng = HaloJacobi((n, n, 2 * n), 2, device_of=dev, exchange="fused", policy="reference")
     assert eng.grid == (1, 1, 2), eng.grid
     out = {"n": n, "grid": eng.grid, "gpus": 2 if a.two_gpus else 1}
-    for zs in (True, False):
+    for mode in ("interior", "slots", "ghost_columns"):
+        zs = mode != "ghost_columns"
         eng.z_slots = zs
+        eng.z_from_interior = mode == "interior"
+        eng.reset()
         for _ in range(3):
             eng.step()
         eng.synchronize()
@@ -37,7 +41,7 @@ def main():
         eng.synchronize()
         eng.check_errors()
         conc = [x.elapsed_time(y) for x, y in timing["exchange"]]
-        out["zslots" if zs else "ghost_columns"] = {
+        out[mode] = {
             "shell_alone_ms": ms, "face_bytes": 8 * n * n,
             "nvlink_gbs": 8 * n * n / (ms * 1e-3) / 1e9,
             "step_ms": e0.elapsed_time(e1) / 10, "shell_concurrent_ms": sum(conc) / len(conc)}
