@@ -25,9 +25,14 @@ and a sequence of them can be captured in a CUDA graph and replayed with no
 host involvement (``osu.channel_latency`` / ``channel_bandwidth`` do exactly
 that).
 
-Kernels: hx_chan_send / hx_chan_recv (include/hx.h). The two endpoints must
-be on different GPUs: a receive spins until its matching send lands, and
-spinning kernels never wait on work queued on their own GPU.
+Kernels: hx_chan_send / hx_chan_recv (include/hx.h). The two endpoints are
+normally on different GPUs: a receive spins until its matching send lands.
+Both on one GPU (two streams) is opt-in (allow_same_gpu) and relies on the
+spinning receive and the send being resident together, which the bounded
+grids allow. A pulled send (larger than a slot) completes only after its
+receive has run, so two pulled sends crossing in opposite directions must
+not each sit in front of the receive the other one waits for on the same
+stream (put one side's receives first, or on another stream).
 """
 
 from __future__ import annotations
@@ -48,18 +53,24 @@ class PersistentChannel:
     straight from the sender's buffer."""
 
     def __init__(self, gpu_a: int, gpu_b: int, slot_bytes: int = 1 << 20, depth: int = 4,
-                 timeout_s: float = 10.0, tickets: int = 4096):
-        if gpu_a == gpu_b:
-            raise ValueError("a persistent channel joins two different GPUs")
+                 timeout_s: float = 10.0, tickets: int = 4096, allow_same_gpu: bool = False):
+        # Both ends on one GPU (allow_same_gpu, two streams) works when a
+        # spinning receive and the send it waits for can be resident
+        # together — true for the bounded grids used here, but not a
+        # guarantee the hardware gives, so it is opt-in (tests on 1-GPU boxes).
+        if gpu_a == gpu_b and not allow_same_gpu:
+            raise ValueError("a persistent channel joins two different GPUs "
+                             "(allow_same_gpu=True for two streams of one GPU)")
         if slot_bytes < 1 or depth < 1:
             raise ValueError("slot_bytes and depth must be positive")
         self.gpus = (gpu_a, gpu_b)
         self.slot_bytes = slot_bytes
         self.depth = depth
         self.timeout_ns = int(timeout_s * 1e9)
-        _lib.call("hx_enable_peer", gpu_a, gpu_b)
-        _lib.call("hx_enable_peer", gpu_b, gpu_a)
-        for g in (gpu_a, gpu_b):  # no lazy kernel load behind a spinning one
+        if gpu_a != gpu_b:
+            _lib.call("hx_enable_peer", gpu_a, gpu_b)
+            _lib.call("hx_enable_peer", gpu_b, gpu_a)
+        for g in sorted({gpu_a, gpu_b}):  # no lazy kernel load behind a spinning one
             _lib.call("hx_set_device", g)
             _lib.call("hx_preload")
         # a slot: header block, then the payload (LL words are 2x the bytes)

@@ -562,3 +562,53 @@ def test_fused_z_faces_from_the_interior_sweep_bitexact(pkg, dims, pes):
     got = [max(eng.residuals(r)[i] for r in eng.blocks) for i in range(3)]
     assert got == wres[:3]
     eng.close()
+
+
+def test_persistent_channel_two_streams_one_gpu(pkg):
+    """pchannel.PersistentChannel with both endpoints on cuda:0 (two streams):
+    LL, slot and pulled messages in both directions, interleaved, in order,
+    bit-exact, with truncation — the device channel kernels on a 1-GPU box."""
+    from paper_2102_12416_b200.completion import OK, TRUNCATED
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    rng = np.random.default_rng(5)
+    slot = 70000
+    ch = PersistentChannel(0, 0, slot_bytes=slot, depth=4, timeout_s=20, allow_same_gpu=True)
+    s = [torch.cuda.Stream(device=0), torch.cuda.Stream(device=0)]
+    # both directions at once: messages that fit a slot (a pulled send waits
+    # for its receive, so two crossing pulls on two streams would each wait
+    # behind the other's send); the pulled sizes go one way, below
+    sizes = [8, 0, 4096, 8193, slot, 1, 65000, 17, 12345]
+    msgs = [[torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8)).to("cuda:0") for n in sizes]
+            for _ in (0, 1)]
+    sinks = [[torch.zeros(max(sizes), dtype=torch.uint8, device="cuda:0") for _ in sizes]
+             for _ in (0, 1)]
+    tickets = [[], []]
+    for k, n in enumerate(sizes):
+        for e in (0, 1):
+            ch.send(e, msgs[e][k], n, stream=s[e])
+        for e in (0, 1):
+            tickets[e].append(ch.recv(1 - e, sinks[e][k], max(sizes), stream=s[1 - e]))
+    ch.check()
+    for e in (0, 1):
+        for k, n in enumerate(sizes):
+            st, length = ch.completion(1 - e, tickets[e][k], max(sizes))
+            assert st == OK and length == n, (e, k)
+            assert torch.equal(sinks[e][k][:n].cpu(), msgs[e][k].cpu()), (e, k)
+    small = torch.zeros(10, dtype=torch.uint8, device="cuda:0")
+    ch.send(0, msgs[0][4], slot, stream=s[0])
+    t = ch.recv(1, small, 10, stream=s[1])
+    assert ch.completion(1, t, 10) == (TRUNCATED, slot)
+    assert torch.equal(small.cpu(), msgs[0][4][:10].cpu())
+    # pulled messages (larger than a slot), endpoint 0 -> 1, mixed with small ones
+    big = [3 << 18, 8, 5 << 20, 70001]
+    src = [torch.from_numpy(rng.integers(0, 256, n, dtype=np.uint8)).to("cuda:0") for n in big]
+    dst = [torch.zeros(n, dtype=torch.uint8, device="cuda:0") for n in big]
+    tk = []
+    for k, n in enumerate(big):
+        ch.send(0, src[k], n, stream=s[0])
+        tk.append(ch.recv(1, dst[k], n, stream=s[1]))
+    for k, n in enumerate(big):
+        assert ch.completion(1, tk[k], n) == (OK, n)
+        assert torch.equal(dst[k].cpu(), src[k].cpu()), k
+    ch.check()
