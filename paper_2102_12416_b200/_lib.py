@@ -13,7 +13,8 @@ import os
 import subprocess
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libhx.so")
+# HX_LIB_PATH: load another build of the same ABI (A/B experiments in tools/)
+LIB_PATH = os.environ.get("HX_LIB_PATH") or os.path.join(_HERE, "libhx.so")
 CSRC = os.path.join(_HERE, "csrc")
 
 HX_E_INVALID = -1
