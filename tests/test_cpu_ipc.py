@@ -240,3 +240,62 @@ def test_ipc_backend_needs_a_process_group(bad):
         pytest.skip("a process group is already initialised")
     with pytest.raises(StartupError):
         TransportGroup(RuntimeConfig(workers=2, backend="ipc"), backend="ipc")
+
+
+def _mesh_worker(rank, world, port, digest, out):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    from paper_2102_12416_b200.wire import LayoutMismatchError, Mesh
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mesh = Mesh(rank, world, digest, dist, timeout_s=30)
+    except LayoutMismatchError as e:
+        out.put((rank, "mismatch", str(e)))
+        dist.destroy_process_group()
+        return
+    sizes = [0, 1, 7, 1 << 16, (1 << 20) + 3, 3 << 20]  # across the 1 MiB receive chunks
+    for k, n in enumerate(sizes):
+        mesh.send(1 - rank, 4, (rank, k, bytes([(k + rank) % 251]) * n))
+    got = []
+    import time
+
+    t0 = time.monotonic()
+    while len(got) < len(sizes) and time.monotonic() - t0 < 60:
+        got += mesh.poll()
+    while not mesh.flushed:
+        mesh.poll()
+    ok = [p == 1 - rank and kind == 4 and b[0] == 1 - rank and b[1] == k and
+          b[2] == bytes([(k + 1 - rank) % 251]) * sizes[k]
+          for k, (p, kind, b) in enumerate(got)]
+    dist.barrier()
+    mesh.close()
+    out.put((rank, "frames", (len(got), all(ok), mesh.frames_sent, mesh.frames_received)))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("same_digest", [True, False])
+def test_wire_mesh_frames_and_digest(same_digest):
+    """wire.Mesh between two processes: frames of 0 B to 3 MiB (across the
+    1 MiB receive chunks) arrive complete and in order both ways; a tag
+    layout digest mismatch in the hello raises LayoutMismatchError
+    (cl/transport.py:77-91)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    digests = [0x1234, 0x1234 if same_digest else 0x9999]
+    procs = [ctx.Process(target=_mesh_worker, args=(r, 2, port, digests[r], q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    if same_digest:
+        for rank, kind, val in res:
+            assert kind == "frames" and val[0] == 6 and val[1], (rank, val)
+            assert val[2] == 6 and val[3] == 6
+    else:
+        assert all(kind == "mismatch" for _, kind, _ in res)
