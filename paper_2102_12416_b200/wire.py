@@ -72,6 +72,7 @@ class Mesh:
         self.conns: dict[int, _Conn] = {}
         self.frames_sent = 0
         self.frames_received = 0
+        self.eof_from: set = set()  # processes whose connection reached end of file
         if world == 1:
             return
         lst = socket.socket(socket.AF_INET, socket.SOCK_STREAM)
@@ -140,11 +141,11 @@ class Mesh:
         every complete frame received since the last poll."""
         out = []
         for conn in self.conns.values():
-            if conn.closed:
+            if conn.closed and not conn.rbuf:
                 continue
-            if conn.wbuf:
+            if conn.wbuf and not conn.closed:
                 self._flush(conn)
-            while True:
+            while not conn.closed:
                 try:
                     chunk = conn.sock.recv(1 << 20)
                 except BlockingIOError:
@@ -152,8 +153,9 @@ class Mesh:
                 except OSError as e:
                     conn.closed = True
                     raise WireError(f"connection to process {conn.peer} failed: {e}") from e
-                if not chunk:
+                if not chunk:  # the peer closed: frames already buffered still parse
                     conn.closed = True
+                    self.eof_from.add(conn.peer)
                     break
                 conn.rbuf += chunk
                 if len(chunk) < (1 << 20):
