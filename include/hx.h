@@ -214,7 +214,8 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
  * neighbour's slot written (its parity q ^ 1 slot); NULL: ghost columns. The same
  * flag protocol as hx_shell_put, so runs may alternate with fused steps. barrier: two
  * zero-initialised uint32 (count, generation). max_ctas caps the grid (every
- * CTA must be co-resident with the other blocks' kernels on this GPU). */
+ * CTA must be co-resident with the other blocks' kernels on this GPU). Blocks
+ * above 2^31 cells: HX_E_INVALID. */
 int hx_persist_run(double *const field[2], double *const peer[12], int bx, int by, int bz,
                    int parity, unsigned long long it0, int iters,
                    unsigned long long *const wait_flag[6], unsigned long long *const signal_flag[6],

@@ -1045,7 +1045,7 @@ face_tma_kernel(const __grid_constant__ CUtensorMap mapx, const __grid_constant_
 // boundary of it-1 is in our ghost planes, and they are done reading the
 // ghosts we are about to write), relaxes the whole block — storing each
 // neighbour-facing cell also into the neighbour's next-buffer ghost plane,
-// as hx_shell_put does — then a grid barrier, and one thread releases
+// as hx_shell_put does — then a grid barrier, and CTA 0 releases
 // flag = it + 2 to every neighbour. Grid-wide barriers need every CTA
 // resident: the host sizes the grid to fit (hx_persist_run).
 struct PersistJob {
@@ -1062,72 +1062,81 @@ struct PersistJob {
     double *zout[2][2];
 };
 
+// One grid-wide barrier: the last CTA to arrive resets the count and bumps
+// the generation (release); the others spin on it (acquire).
 __device__ __forceinline__ void grid_barrier(unsigned *count, unsigned *gen) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        const unsigned g = *(volatile unsigned *)gen;
-        __threadfence();
-        if (atomicAdd(count, 1u) + 1u == gridDim.x) {
-            *count = 0u;
-            __threadfence();
-            atomicAdd(gen, 1u);  // release the others
+        unsigned g, prev;
+        asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+        asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;"
+                     : "=r"(prev) : "l"(count) : "memory");
+        if (prev + 1u == gridDim.x) {
+            asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(count) : "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(gen) : "memory");
         } else {
-            while (*(volatile unsigned *)gen == g) __nanosleep(32);
+            unsigned v;
+            do {
+                asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(gen) : "memory");
+            } while (v == g);
         }
-        __threadfence();
     }
     __syncthreads();
 }
 
+// One grid barrier per iteration. Every CTA acquires the neighbours' flags
+// itself (threads 0-5, one flag each), so no barrier is needed to hand
+// CTA 0's acquires to the grid; the barrier after the sweep orders every
+// CTA's local and peer stores before CTA 0's release, and also closes the
+// iteration for the local buffers (the next one writes what this one read).
+// A timed-out wait skips the sweep but still arrives, so nobody hangs.
 __global__ void __launch_bounds__(256)
 persist_kernel(PersistJob J, int bx, int by, int bz, int parity, unsigned long long it0, int iters,
                unsigned *bar_count, unsigned *bar_gen, unsigned long long timeout_ns, int *err) {
-    __shared__ int ok;
     const hx::Geom g(by, bz);
-    const size_t sx = (size_t)g.py * g.pz, sy = g.pz;
-    const long long cells = (long long)bx * by * bz;
+    const unsigned sx = (unsigned)(g.py * g.pz), sy = (unsigned)g.pz;
+    const unsigned cells = (unsigned)bx * by * bz;  // the host keeps blocks below 2^31 cells
     for (int n = 0; n < iters; ++n) {
         const unsigned long long it = it0 + n;
         const int p = (parity + n) & 1;
-        if (threadIdx.x == 0) {
-            ok = 1;
-            if (blockIdx.x == 0)
-                for (int d = 0; d < 6 && ok; ++d)
-                    if (J.wait[d]) ok = hx::spin_until(J.wait[d], it + 1, timeout_ns, err);
-        }
-        grid_barrier(bar_count, bar_gen);  // CTA 0's acquires -> every CTA
-        if (err && *(volatile int *)err) return;  // a timed-out wait: everyone stops
-        const double *cur = J.field[p];
-        double *nxt = J.field[p ^ 1];
-        for (long long q = blockIdx.x * (long long)blockDim.x + threadIdx.x; q < cells;
-             q += (long long)gridDim.x * blockDim.x) {
-            const int k = 1 + (int)(q % bz);
-            const long long r = q / bz;
-            const int j = 1 + (int)(r % by), i = 1 + (int)(r / by);
-            const size_t c = g.at(i, j, k);
+        int ok = 1;
+        if (threadIdx.x < 6 && J.wait[threadIdx.x])
+            ok = hx::spin_until(J.wait[threadIdx.x], it + 1, timeout_ns, err, 32);
+        ok = __syncthreads_and(ok);
+        if (ok && !(err && *(volatile int *)err)) {
+            const double *cur = J.field[p];
+            double *nxt = J.field[p ^ 1];
             const int qi = (int)(it & 1);  // zin[qi]: this iteration's slots; zout[qi]: the
                                            // neighbour's slots for the next one
-            const size_t packed = (size_t)(i - 1) * by + (j - 1);
-            const double zm = (k == 1 && J.zin[qi][0]) ? J.zin[qi][0][packed] : cur[c - 1];
-            const double zp = (k == bz && J.zin[qi][1]) ? J.zin[qi][1][packed] : cur[c + 1];
-            const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy], zm, zp));
-            nxt[c] = v;
-            const int at[3] = {i, j, k};
+            for (unsigned q = blockIdx.x * blockDim.x + threadIdx.x; q < cells;
+                 q += gridDim.x * blockDim.x) {
+                const unsigned r = q / (unsigned)bz;
+                const int k = 1 + (int)(q - r * (unsigned)bz);
+                const unsigned i0 = r / (unsigned)by;
+                const int j = 1 + (int)(r - i0 * (unsigned)by), i = 1 + (int)i0;
+                const size_t c = (size_t)i * sx + (size_t)j * sy + k;
+                const unsigned packed = r;  // (i - 1) * by + (j - 1)
+                const double zm = (k == 1 && J.zin[qi][0]) ? J.zin[qi][0][packed] : cur[c - 1];
+                const double zp = (k == bz && J.zin[qi][1]) ? J.zin[qi][1][packed] : cur[c + 1];
+                const double v = div6(sum6(cur[c - sx], cur[c + sx], cur[c - sy], cur[c + sy], zm, zp));
+                nxt[c] = v;
+                const int at[3] = {i, j, k};
 #pragma unroll
-            for (int d = 0; d < 6; ++d)
-                if (J.peer[d][p ^ 1] && at[d >> 1] == J.face[d]) {
-                    if (d >= 4 && J.zout[qi][d - 4])
-                        J.zout[qi][d - 4][packed] = v;
-                    else
-                        J.peer[d][p ^ 1][(long long)c + J.shift[d]] = v;
-                }
+                for (int d = 0; d < 6; ++d)
+                    if (J.peer[d][p ^ 1] && at[d >> 1] == J.face[d]) {
+                        if (d >= 4 && J.zout[qi][d - 4])
+                            J.zout[qi][d - 4][packed] = v;
+                        else
+                            J.peer[d][p ^ 1][(long long)c + J.shift[d]] = v;
+                    }
+            }
         }
         grid_barrier(bar_count, bar_gen);  // every CTA's local + peer stores are done
-        if (blockIdx.x == 0 && threadIdx.x == 0) {
-            __threadfence_system();
-            for (int d = 0; d < 6; ++d)
-                if (J.signal[d]) hx::st_release_sys(J.signal[d], it + 2);
-        }
+        if (err && *(volatile int *)err) return;  // a timed-out wait: everyone stops
+        // CTA 0 releases the six flags in parallel (each st.release.sys is
+        // cumulative over the stores the grid barrier ordered before it)
+        if (blockIdx.x == 0 && threadIdx.x < 6 && J.signal[threadIdx.x])
+            hx::st_release_sys(J.signal[threadIdx.x], it + 2);
     }
 }
 
@@ -1814,7 +1823,7 @@ int hx_persist_run(double *const field[2], double *const peer[12], int bx, int b
                    const double *const zin[4], double *const zout[4], unsigned *barrier,
                    int max_ctas, unsigned long long timeout_ns, int *err, void *stream) {
     if (!field || !field[0] || !field[1] || !barrier || bx < 1 || by < 1 || bz < 1 ||
-        iters < 0 || (parity & ~1))
+        iters < 0 || (parity & ~1) || (long long)bx * by * bz > (1LL << 31))
         return HX_E_INVALID;
     if (iters == 0) return 0;
     PersistJob J;
