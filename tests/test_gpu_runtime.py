@@ -539,6 +539,29 @@ def test_persistent_kernel_run_bitexact(pkg, dims, pes):
     eng.close()
 
 
+def test_persistent_kernel_timeout_stops_every_cta(pkg):
+    """A neighbour that never runs: every CTA's flag wait times out, still
+    arrives at the grid barrier, and the launch ends with HX_E_TIMEOUT in the
+    block's error word instead of hanging the GPU."""
+    import time
+
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi((48, 40, 32), 2, device_of=lambda r: 0, exchange="fused", timeout_s=0.5)
+    eng.step()  # both blocks: flags for iteration 1 released
+    both = eng.blocks
+    eng.blocks = {0: both[0]}  # block 1 never runs: block 0 waits at iteration 2
+    t0 = time.perf_counter()
+    eng.run_persistent(4)
+    eng.synchronize()
+    elapsed = time.perf_counter() - t0
+    eng.blocks = both
+    assert elapsed < 20, elapsed
+    with pytest.raises(RuntimeError, match="block 0: device error"):
+        eng.check_errors()
+    eng.close()
+
+
 @pytest.mark.parametrize("dims,pes", [((32, 40, 64), 2), ((48, 48, 48), 8), ((40, 32, 96), 4)])
 def test_fused_z_faces_from_the_interior_sweep_bitexact(pkg, dims, pes):
     """The alternative z-face path (HaloJacobi.z_from_interior: hx_stencil_box_z
