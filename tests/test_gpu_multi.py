@@ -377,6 +377,38 @@ def test_persistent_channel_random_schedules(cuda, seed):
 
 
 @needs2
+def test_persistent_channel_saturated_both_directions(cuda):
+    """Both GPUs send 16 pulled 16 MiB messages while receiving 16 (the
+    largest receive grids: up to 2 x SMs spinning CTAs per GPU, plus the
+    sends), each endpoint on a send stream and a receive stream. Every sink
+    must equal its source; no wait may time out."""
+    from paper_2102_12416_b200.pchannel import PersistentChannel
+
+    n, size = 16, 16 << 20
+    ch = PersistentChannel(0, 1, slot_bytes=64 << 10, depth=4, timeout_s=20)
+    send_s = [torch.cuda.Stream(device=e) for e in (0, 1)]
+    recv_s = [torch.cuda.Stream(device=e) for e in (0, 1)]
+    gens = [torch.Generator(device=f"cuda:{e}").manual_seed(7 + e) for e in (0, 1)]
+    srcs = [[torch.randint(0, 256, (size,), dtype=torch.uint8, device=f"cuda:{e}",
+                           generator=gens[e]) for _ in range(n)] for e in (0, 1)]
+    sinks = [[torch.zeros(size, dtype=torch.uint8, device=f"cuda:{1 - e}") for _ in range(n)]
+             for e in (0, 1)]
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    for k in range(n):  # interleave the two directions' sends and receives
+        for e in (0, 1):
+            ch.send(e, srcs[e][k], stream=send_s[e])
+            ch.recv(1 - e, sinks[e][k], stream=recv_s[1 - e])
+    torch.cuda.synchronize(0)
+    torch.cuda.synchronize(1)
+    ch.check()
+    for e in (0, 1):
+        for k in range(n):
+            assert torch.equal(sinks[e][k].cpu(), srcs[e][k].cpu()), (e, k)
+    assert ch.counters == [(n, n), (n, n)]
+
+
+@needs2
 @pytest.mark.parametrize("dims", [(48, 32, 40), (32, 48, 40), (32, 32, 64)])
 def test_nccl_comparison_exchange_bitexact(cuda, tmp_path, dims):
     """The north star's comparison point (HaloJacobi(exchange="nccl"): pack,
