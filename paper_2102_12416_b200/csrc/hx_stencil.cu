@@ -1194,12 +1194,16 @@ int tensor_map_for(const double *cur, int bx, int by, int bz, int box_z, CUtenso
 }
 
 // Tensor map over the padded block with an arbitrary 3-D box (the face
-// kernel's x-slab and y-slab boxes), cached like tensor_map_for's.
-std::map<std::tuple<const void *, int, int, int, int, int, int>, CUtensorMap> g_face_maps;
+// kernel's x-slab, y-slab and z-tile boxes), cached like tensor_map_for's.
+// promo is the L2 promotion (0 none .. 3 256 B): the x/y boxes read whole
+// 132-double row segments (256 B, as the stencil), but a z-tile row is 4
+// doubles 12 KB from the next, and promoting it to 256 B would fetch 8x
+// the bytes it uses from DRAM.
+std::map<std::tuple<const void *, int, int, int, int, int, int, int>, CUtensorMap> g_face_maps;
 
-int face_map_for(const double *cur, int bx, int by, int bz, int b0, int b1, int b2,
+int face_map_for(const double *cur, int bx, int by, int bz, int b0, int b1, int b2, int promo,
                  CUtensorMap *out) {
-    auto key = std::make_tuple((const void *)cur, bx, by, bz, b0, b1, b2);
+    auto key = std::make_tuple((const void *)cur, bx, by, bz, b0, b1, b2, promo);
     {
         std::lock_guard<std::mutex> lk(g_map_mu);
         auto it = g_face_maps.find(key);
@@ -1218,7 +1222,7 @@ int face_map_for(const double *cur, int bx, int by, int bz, int b0, int b1, int 
     CUtensorMap m;
     CUresult r = encode(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void *)cur, dims, strides, box,
                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        (CUtensorMapL2promotion)promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return HX_E_TMA;
     std::lock_guard<std::mutex> lk(g_map_mu);
     if (g_face_maps.size() > 256) g_face_maps.clear();
@@ -1652,6 +1656,8 @@ int hx_preload_halo_kernels();  // hx_halo.cu
 // front on the current device (the stencil variants are launched alone or
 // concurrently with the fused shell, which needs no other kernel to finish).
 int hx_preload() {
+    if (const char *e = getenv("HX_L2_FETCH"))  // measurement knob: L2 fetch granularity (bytes)
+        HX_TRY(cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, (size_t)atoi(e)));
     cudaFuncAttributes a;
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)shell_put_kernel));
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)face_tma_kernel));
@@ -1778,9 +1784,14 @@ int hx_shell_put_z(const double *cur, double *nxt, int bx, int by, int bz, int n
             F.signal[d] = J.signal[d];
         }
         CUtensorMap mx, my, mz;
-        if (int rc = face_map_for(cur, bx, by, bz, FBK, FBR, 3, &mx)) return rc;
-        if (int rc = face_map_for(cur, bx, by, bz, FBK, 3, FBR, &my)) return rc;
-        if (int rc = face_map_for(cur, bx, by, bz, ZBK, ZBJ, ZBI, &mz)) return rc;
+        static int zpromo = -1;  // z-tile L2 promotion (HX_FACE_ZPROMO, 0..3; default none)
+        if (zpromo < 0) {
+            const char *e = getenv("HX_FACE_ZPROMO");
+            zpromo = e ? std::min(3, std::max(0, atoi(e))) : 0;
+        }
+        if (int rc = face_map_for(cur, bx, by, bz, FBK, FBR, 3, l2_promotion(), &mx)) return rc;
+        if (int rc = face_map_for(cur, bx, by, bz, FBK, 3, FBR, l2_promotion(), &my)) return rc;
+        if (int rc = face_map_for(cur, bx, by, bz, ZBK, ZBJ, ZBI, zpromo, &mz)) return rc;
         static unsigned long long attr_set = 0;
         if (int rc = ensure_smem(face_tma_kernel, FACE_SMEM, attr_set)) return rc;
         static int face_bulk = -1;  // bulk-copy row segments to the peer (HX_FACE_BULK=0: plain stores)

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     args = ap.parse_args()
     n = args.n
+    _lib.call("hx_preload")  # (applies HX_L2_FETCH, if set)
     f = torch.randn((n + 2,) * 3, dtype=torch.float64, device="cuda")
     slot = torch.empty(n * n, dtype=torch.float64, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
