@@ -63,6 +63,52 @@ def _round(n: int) -> int:
     return (n + _ALIGN - 1) // _ALIGN * _ALIGN
 
 
+_STAGING: dict = {}
+
+
+def _staging(nbytes: int, count: int) -> list:
+    """Process-wide ring of ``count`` pinned byte buffers of at least
+    ``nbytes`` (interior_into's read-back staging)."""
+    ring = _STAGING.get(count)
+    if ring is None or ring[0].numel() < nbytes:
+        ring = _STAGING[count] = [torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+                                  for _ in range(count)]
+    return ring
+
+
+def _split(n: int, parts: int) -> list:
+    """[r0, r1) ranges cutting range(n) into at most ``parts`` near-equal pieces."""
+    parts = max(1, min(parts, n))
+    return [(n * p // parts, n * (p + 1) // parts) for p in range(parts)]
+
+
+def _copy_rows(out, host, i0: int, r0: int, r1: int, by: int) -> None:
+    """Copy interior rows [r0, r1) (flattened (plane, row)) of the padded
+    planes ``host`` (k, by + 2, bz + 2) into ``out[i0 + plane, row]``."""
+    while r0 < r1:
+        a, j0 = divmod(r0, by)
+        j1 = min(by, j0 + (r1 - r0))
+        np.copyto(out[i0 + a, j0:j1], host[a, 1 + j0:1 + j1, 1:-1])
+        r0 += j1 - j0
+
+
+def prefault_host(shape, threads: int = 16):
+    """A float64 host array of ``shape`` whose pages are being touched by
+    ``threads`` background threads (returns (array, futures)). First touch
+    of fresh pages (the kernel zeroes them) is the slow part of reading a
+    large field back (~6 GB/s per thread); run_jacobi starts it before the
+    iterations so it overlaps the GPU work."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    out = np.empty(shape)
+    flat = out.reshape(-1)
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1
+    pool = ThreadPoolExecutor(max(1, min(threads, cores)))
+    futs = [pool.submit(flat[a:b].fill, 0.0) for a, b in _split(flat.size, max(1, min(threads, cores)))]
+    pool.shutdown(wait=False)
+    return out, futs
+
+
 class HaloBlock:
     """One block: two padded fields + its receive arena on one GPU."""
 
@@ -230,7 +276,6 @@ class HaloJacobi:
         self._ipc_bases = []
         self._res = {}
         self._graphs = {}  # buffer parity -> {device: CUDAGraph} (run_graph)
-        self._stages = {}  # pinned read-back staging (interior_into)
         self.reset()
         if exchange in ("p2p", "fused"):
             self.connect()
@@ -919,40 +964,40 @@ class HaloJacobi:
 
     def interior_into(self, rank: int, out: np.ndarray) -> None:
         """Copy block ``rank``'s current interior into the host array view
-        ``out`` (shape (bx, by, bz), any strides): x-plane chunks of about
-        256 MB go device -> pinned staging (two buffers, the next chunk's
-        copy overlaps the previous chunk's host copy), and host threads
-        spread each chunk into ``out`` — ~10x a pageable .cpu() of a
-        29 GB block plus a second host copy into the assembled field."""
+        ``out`` (shape (bx, by, bz), any strides): chunks of whole padded
+        x planes (about 64 MB, contiguous in HBM, so one plain D2H each) go
+        device -> pinned staging (a ring of three, so two chunks' host
+        copies overlap the next chunk's transfer), and host threads spread
+        each chunk's interior rows into ``out``. The staging ring is kept per process
+        (pinned allocation is slow). 1536^3 (29 GB): ~1.0 s with 16 threads,
+        against ~21 s for a pageable .cpu() plus a second host copy; the
+        host side (first touch of the output's pages) is the bound, PCIe
+        D2H runs at ~49 GB/s (tools/prof_readback.py, tools/prof_pcie.py)."""
         from concurrent.futures import ThreadPoolExecutor
 
         b = self.blocks[rank]
-        src = b.fields[b.cur][1:-1, 1:-1, 1:-1]
+        field = b.fields[b.cur]  # whole padded planes are contiguous: one plain D2H per chunk
         s = self.stream_of(b)
-        plane = b.by * b.bz * 8
-        per = max(1, min(b.bx, (256 << 20) // plane))
-        key = (per, b.by, b.bz)
-        stages = self._stages.get(key)
-        if stages is None:
-            stages = self._stages[key] = [
-                torch.empty((per, b.by, b.bz), dtype=torch.float64, pin_memory=True) for _ in range(2)]
-        nthreads = max(1, min(8, (len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity")
-                                  else os.cpu_count() or 1)))
+        py, pz = b.by + 2, b.bz + 2
+        plane = py * pz * 8
+        per = max(1, min(b.bx, (64 << 20) // plane))
+        stages = _staging(per * plane, 3)
+        cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1
+        nthreads = max(1, min(int(os.environ.get("HX_READBACK_THREADS", 16)), cores))
         with ThreadPoolExecutor(nthreads) as pool:
-            pending = [[], []]
+            pending = [[] for _ in stages]
             with torch.cuda.device(b.device), torch.cuda.stream(s):
                 for c, i in enumerate(range(0, b.bx, per)):
                     k = min(per, b.bx - i)
-                    for f in pending[c % 2]:  # the staging buffer's previous chunk is out
+                    q = c % len(stages)
+                    for f in pending[q]:  # the staging buffer's previous chunk is out
                         f.result()
-                    st = stages[c % 2]
-                    st[:k].copy_(src[i:i + k], non_blocking=True)
+                    st = stages[q][: k * plane].view(torch.float64).view(k, py, pz)
+                    st.copy_(field[1 + i:1 + i + k], non_blocking=True)
                     s.synchronize()
-                    host = st.numpy()
-                    step = max(1, -(-k // nthreads))
-                    pending[c % 2] = [pool.submit(np.copyto, out[i + a:i + min(a + step, k)],
-                                                  host[a:min(a + step, k)])
-                                      for a in range(0, k, step)]
+                    host = st.numpy()  # ghost rows and columns are dropped by the host copy
+                    pending[q] = [pool.submit(_copy_rows, out, host, i, r0, r1, b.by)
+                                  for r0, r1 in _split(k * b.by, nthreads)]
             for fs in pending:
                 for f in fs:
                     f.result()
@@ -961,10 +1006,15 @@ class HaloJacobi:
         self.synchronize()
         return [float(t.cpu().numpy().view(np.float64)[0]) for t in self._res.get(rank, [])]
 
-    def assemble(self) -> np.ndarray:
+    def assemble(self, out: np.ndarray | None = None) -> np.ndarray:
         """Global interior (all blocks must be local), each block copied
-        straight into its slice of the result."""
-        out = np.empty(self.dims)
+        straight into its slice of the result (``out``, if given: a float64
+        array of the global shape, e.g. one whose pages were touched ahead
+        of time by prefault_host)."""
+        if out is None:
+            out = np.empty(self.dims)
+        elif out.shape != tuple(self.dims) or out.dtype != np.float64:
+            raise ValueError(f"out must be float64 {tuple(self.dims)}, got {out.dtype} {out.shape}")
         bx, by, bz = (self.dims[a] // self.grid[a] for a in range(3))
         for r in range(self.pes):
             ix, iy, iz = _block_coords(r, self.grid)

@@ -185,6 +185,22 @@ def test_reference_acceptance_64cubed_100_iters_all_modes(cuda, pes):
         assert (r["comm_ns"] == 0.0) == (pes == 1), (mode, pes)
 
 
+@pytest.mark.parametrize("pes", [1, 2])
+def test_run_jacobi_large_field_prefaulted_readback_vs_c_oracle(oracle_c, pes):
+    """run_jacobi on a field above the prefault threshold (512^3 = 1.07 GB):
+    the result array is touched on host threads while the GPU iterates, then
+    read back chunk by chunk through the pinned staging ring; it must equal
+    the C oracle's sequential sweep bit for bit."""
+    from paper_2102_12416_b200 import jacobi3d
+
+    dims, iters = (512, 512, 512), 4
+    assert 8 * 512 ** 3 >= jacobi3d._PREFAULT_MIN_BYTES
+    r = jacobi3d.run_jacobi(dims=dims, iters=iters, mode="channel-persistent", pes=pes)
+    want, _ = oracle_c.sequential(dims, iters)
+    assert r["field"].shape == dims
+    assert np.array_equal(r["field"].view(np.uint64), want.view(np.uint64))
+
+
 @pytest.mark.parametrize("mode", ["0", "fused", "graph"])
 def test_ipc_engine_two_processes_one_gpu(cuda, tmp_path, mode):
     """torchrun, 2 ranks, both on cuda:0: arenas and fields exported with
