@@ -1602,29 +1602,28 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
     Z.err = err;
     g_last_variant = 1;
     cudaStream_t st = (cudaStream_t)stream;
-    // Only the tile columns that hold k = 1 or k = bz take the z-edge kernel
-    // (more registers, a flag wait, slot patches): the middle columns are a
-    // plain interior sweep on the same tile grid, launched first.
+    // Only the tile columns that hold k = 1 (with a -z neighbour) or k = bz
+    // (with a +z neighbour) take the z-edge kernel (more registers, a flag
+    // wait, slot patches); the rest is one plain sweep on the same tile grid,
+    // launched first. A narrow strip sweep runs at about half the HBM rate
+    // (each tile row opens its own DRAM page), so a side without a z
+    // neighbour stays in the main sweep (ncu: profiles/r2_zface_dram.md).
     const int klo_end = 1 + TZ;                       // the first tile column: [1, 1 + TZ)
     const int khi_beg = 1 + ((bz - 1) / TZ) * TZ;     // the tile column holding k = bz
     if (khi_beg <= klo_end) {  // one or two tile columns: everything is an edge
         return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, bz + 1, res, st, &Z);
     }
-    if (khi_beg > klo_end)
-        if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, klo_end, khi_beg, res, st))
-            return rc;
+    const int mid0 = Z.flag[0] ? klo_end : 1, mid1 = Z.flag[1] ? khi_beg : bz + 1;
+    if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, mid0, mid1, res, st)) return rc;
     ZEdge lo = Z, hi = Z;
     lo.flag[1] = nullptr;
     hi.flag[0] = nullptr;
-    if (Z.flag[0]) {
+    if (Z.flag[0])
         if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, klo_end, res, st, &lo))
             return rc;
-    } else if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, klo_end, res, st)) {
-        return rc;
-    }
     if (Z.flag[1])
         return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, khi_beg, bz + 1, res, st, &hi);
-    return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, khi_beg, bz + 1, res, st);
+    return 0;
 }
 
 // After a fused step's interior and boundary kernels: release the z
