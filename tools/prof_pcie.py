@@ -1,3 +1,9 @@
+"""Host <-> device copy rates on the GPU box: pinned D2H / H2D of 256 MB,
+and first-touch vs warm memset of an 8 GB numpy array (one thread) — the
+ingredients of run_jacobi's field read-back.
+
+    python tools/prof_pcie.py
+"""
 import torch, time, json, os
 x = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 for pin in (True,):
