@@ -539,6 +539,40 @@ def test_persistent_kernel_run_bitexact(pkg, dims, pes):
     eng.close()
 
 
+@pytest.mark.parametrize("dims,pes,policy", [((128, 128, 64), 4, "b200"),
+                                             ((64, 128, 128), 4, "reference")])
+def test_exchange_soak_mixed_schedules_vs_one_block(pkg, dims, pes, policy):
+    """Thousands of fused iterations on a random field — graph replays,
+    persistent runs and eager steps alternating — on every visible GPU (round
+    robin), bitwise equal to one block with no exchange after the same
+    number of iterations (tools/soak.py runs the long version: 20 000
+    iterations, profiles/r2_soak_2gpu.jsonl)."""
+    import torch
+
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    ngpu = max(1, torch.cuda.device_count())
+    eng = HaloJacobi(dims, pes, device_of=lambda r: r % ngpu, exchange="fused", policy=policy,
+                     timeout_s=20)
+    eng.fill_random(5)
+    eng.synchronize()
+    init = eng.assemble()
+    sched = [("eager", 3), ("graph", 1000), ("persistent", 700), ("eager", 2), ("graph", 301)]
+    for how, n in sched:
+        {"eager": eng.run, "graph": eng.run_graph, "persistent": eng.run_persistent}[how](n)
+    eng.check_errors()
+    got = eng.assemble()
+    eng.close()
+    ref = HaloJacobi(dims, 1, device_of=lambda r: 0, exchange="fused", policy=policy)
+    b = ref.blocks[0]
+    b.fields[b.cur][1:-1, 1:-1, 1:-1].copy_(torch.from_numpy(init))
+    torch.cuda.synchronize()
+    ref.run(sum(n for _, n in sched))
+    want = ref.assemble()
+    ref.close()
+    assert got.tobytes() == want.tobytes()
+
+
 def test_persistent_kernel_timeout_stops_every_cta(pkg):
     """A neighbour that never runs: every CTA's flag wait times out, still
     arrives at the grid barrier, and the launch ends with HX_E_TIMEOUT in the
