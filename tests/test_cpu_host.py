@@ -104,3 +104,30 @@ def test_parse_sizes():
     assert parse_sizes("1:10:+4") == [1, 5, 9]
     with pytest.raises(BenchError):
         parse_sizes("1:10:y2")
+
+
+def test_readback_row_split_and_prefault():
+    """The read-back helpers of HaloJacobi.interior_into: _split cuts the
+    rows evenly, _copy_rows drops the staged planes' ghost rows / columns
+    into any strided view of the result, prefault_host returns a touched
+    (zero) array of the global shape."""
+    import numpy as np
+
+    from paper_2102_12416_b200.halo import _copy_rows, _split, prefault_host
+
+    assert _split(10, 3) == [(0, 3), (3, 6), (6, 10)]
+    assert _split(2, 16) == [(0, 1), (1, 2)]
+    assert _split(0, 4) == [(0, 0)]
+    rng = np.random.default_rng(3)
+    k, by, bz = 3, 5, 7
+    host = rng.standard_normal((k, by + 2, bz + 2))
+    glob = np.zeros((4 * k, 2 * by, 3 * bz))
+    view = glob[k:2 * k, by:2 * by, bz:2 * bz]  # a block's slice of the global field
+    for r0, r1 in _split(k * by, 4):
+        _copy_rows(view, host, 0, r0, r1, by)
+    assert np.array_equal(view, host[:, 1:-1, 1:-1])
+    assert glob.sum() == view.sum()
+    out, futs = prefault_host((6, 5, 4), threads=3)
+    for f in futs:
+        f.result()
+    assert out.shape == (6, 5, 4) and out.dtype == np.float64 and not out.any()
