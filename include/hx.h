@@ -228,7 +228,9 @@ int hx_persist_run(double *const field[2], double *const peer[12], int bx, int b
  * read the ghost column from zin[h] (packed [i-1][j-1], bx x by) and copy the
  * face cells into zout[h] (the neighbour's slot for the next step); the rest
  * is hx_stencil_box. The z faces then cost no extra HBM traffic (the sweep
- * stages those rows anyway). Not TMA-eligible or another box: HX_E_INVALID. */
+ * stages those rows anyway). One launch: the edge tiles take the z work at
+ * run time. Not TMA-eligible, another box, or both z neighbours with
+ * bz <= 64 (one tile would hold both faces): HX_E_INVALID. */
 int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int i0, int i1,
                      int j0, int j1, int k0, int k1, unsigned long long *res,
                      const unsigned long long *const zflag[2], const unsigned long long *zstep,

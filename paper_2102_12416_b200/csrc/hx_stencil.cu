@@ -128,20 +128,22 @@ __device__ __forceinline__ void warp_max_to_global(unsigned long long worst,
 // are advanced. Stores the live cells of plane q and folds their residual.
 // ROWSTEP: staged distance between a thread's rows r and r + NWARP; ylo /
 // yhi: distance from a cell to its y-1 / y+1 neighbour in P0.
-// ZE: cells p in zmask0 / zmask1 are also copied to zdst0 / zdst1 (+ the
-// row offset): a z face produced by the interior sweep (ZEdge below).
+// ZS (1: the tile holds k = 1 with a -z neighbour, 2: k = bz with a +z
+// neighbour): on the edge lane (zedge, half zc) the z ghost is zg[row] and
+// the cell is also copied to zdst[row] — the z faces produced by the
+// interior sweep (ZEdge below).
 // CONSEC: the thread's ROWS rows are consecutive (ROWSTEP = one staged
 // row), so an inner row's y neighbours are the rows above / below it that
 // the thread already holds in registers (x0: plane q's values): 2 of the 8
 // y loads per row pair stay in shared memory instead of 8 — 28 shared loads
 // per 8 cells instead of 40 (less shared-memory traffic per cell).
-template <bool RES, int ROWSTEP, bool ZE = false, bool CONSEC = false>
+template <bool RES, int ROWSTEP, int ZS = 0, bool CONSEC = false>
 __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, int soff, int ylo,
                                             int yhi, double (&xm)[PTS], double (&x0)[PTS],
                                             double *out, int bz, unsigned live,
-                                            unsigned long long &worst, double *zdst0 = nullptr,
-                                            unsigned zmask0 = 0, double *zdst1 = nullptr,
-                                            unsigned zmask1 = 0, int zrow = 0) {
+                                            unsigned long long &worst, bool zedge = false,
+                                            int zc = 0, const double *zg = nullptr,
+                                            double *zdst = nullptr) {
     double v[PTS];
     bool fast = true;
     double prev[2] = {0.0, 0.0};  // CONSEC: row t - 1's plane-q values
@@ -159,7 +161,12 @@ __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, 
             ym = P0[o - ylo];
             yp = P0[o + yhi];
         }
-        v[p] = sum6(xm[p], xp, ym, yp, P0[o - 1], P0[o + 1]);
+        double zm = P0[o - 1], zp = P0[o + 1];
+        // ZS: the edge lane's z ghost comes from the neighbour's slot (zg,
+        // staged by cp.async), not from the field's ghost column
+        if (ZS == 1 && zedge && c == zc) zm = zg[t];
+        if (ZS == 2 && zedge && c == zc) zp = zg[t];
+        v[p] = sum6(xm[p], xp, ym, yp, zm, zp);
         xm[p] = x0[p];
         x0[p] = xp;
         fast &= div6_fast_ok(v[p]);
@@ -177,10 +184,7 @@ __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, 
             constexpr int RS = CONSEC ? 1 : NWARP;  // rows between a thread's rows
             out[(size_t)((p >> 1) * RS) * (bz + 2) + 32 * (p & 1)] = v[p];
             if (RES) worst = max(worst, abs_diff_bits(v[p], xm[p]));
-            if (ZE) {
-                if ((zmask0 >> p) & 1u) zdst0[(p >> 1) * RS * zrow] = v[p];
-                if ((zmask1 >> p) & 1u) zdst1[(p >> 1) * RS * zrow] = v[p];
-            }
+            if (ZS && zedge && (p & 1) == zc) zdst[(p >> 1) * RS] = v[p];  // face -> slot
         }
     }
 }
@@ -229,22 +233,22 @@ struct ZEdge {
     int *err;
 };
 
-template <bool RES, int BOX_Z, bool ZE>
-__global__ void __launch_bounds__(THREADS, ZE ? 2 : MIN_CTAS)  // ZE: the edge strips only
-stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__ nxt, int by,
-                   int bz, int i0, int i1, int j0, int j1, int k0, int k1, int klive, int ntj,
-                   int ntk, int chunk, int nchunks, int grows, unsigned long long *res, ZEdge Z) {
+// One work item (tile x chunk) of the TMA sweep. ZE: the tile holds k = 1
+// with a -z neighbour (zlo) or k = bz with a +z neighbour (zhi) and does the
+// z-edge work as well; the kernel picks the instance per tile, so the plain
+// tiles of a z-edge launch run the plain code (and registers).
+template <bool RES, int BOX_Z, int ZS>  // ZS: bit 0 the tile holds k = 1 (-z), bit 1 k = bz (+z)
+__device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restrict__ nxt, int by,
+                                         int bz, int j1, int k1, int klive, const Item &it,
+                                         unsigned long long *res, const ZEdge &Z) {
+    constexpr bool ZE = ZS != 0, zlo = (ZS & 1) != 0, zhi = (ZS & 2) != 0;
     constexpr unsigned STAGE_BYTES = BOX_Y * BOX_Z * sizeof(double);
     extern __shared__ __align__(128) unsigned char smem[];
     uint64_t *bar = reinterpret_cast<uint64_t *>(smem + NSTAGE * STAGE_STRIDE);
 
-    const Item it = work_item(j0, k0, i0, i1, ntj, ntk, chunk, nchunks, grows);
     const int jb = it.jb, kb = it.kb, ib = it.ib, nplanes = it.nplanes;
     const int kshift = BOX_Z == TZ + 2 ? 0 : (kb - 1) & 1;  // 16-byte aligned TMA rows
     const int kload = kb - 1 - kshift;
-    // z-edge tile: holds k = 1 (-z neighbour) / k = bz (+z neighbour)
-    const bool zlo = ZE && Z.flag[0] && kb <= 1 && 1 < kb + TZ && k0 <= 1;
-    const bool zhi = ZE && Z.flag[1] && kb <= bz && bz < kb + TZ && bz < k1;
 
     if (ZE && threadIdx.x == 0 && (zlo || zhi)) {
         const unsigned long long want = *(volatile const unsigned long long *)Z.step + 1;
@@ -276,34 +280,34 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
         if (jb + r < j1 && kb + kk < k1 && kb + kk >= klive) live |= 1u << p;
     }
 
-    // ZE: warp 0 patches the staged plane's z ghost column(s) from the
-    // slots (rows jb .. jb + 31 of padded plane P, relaxed planes only). The
-    // slot values are loaded one plane ahead into registers (zfetch), so the
-    // load latency hides behind the previous plane's relax.
-    const bool zrow = ZE && (zlo || zhi) && warp == 0 && jb + lane <= by;
-    double zg0 = 0.0, zg1 = 0.0;
-    auto zfetch = [&](int P) {  // the slot values of padded plane P (registers)
-        if (!zrow) return;
-        const size_t at = (size_t)(P - 1) * by + (jb + lane - 1);
-        if (zlo) zg0 = Z.zin[0][at];
-        if (zhi) zg1 = Z.zin[1][at];
+    // ZE (ZS = 1: the tile holds k = 1, ZS = 2: k = bz): the neighbour's slot
+    // supplies the edge column's z ghost. Warp 0 stages slot rows jb .. jb+31
+    // of each relaxed plane with cp.async into the unused tail of that
+    // plane's stage (a 66-wide box leaves 608 bytes), two planes ahead; the
+    // per-plane CTA barrier publishes them. The TMA never writes the tail,
+    // so no proxy fence is needed, and nothing stays in registers.
+    constexpr unsigned ZG_OFF = BOX_Y * BOX_Z * sizeof(double);
+    static_assert(!ZE || ZG_OFF + TY * sizeof(double) <= STAGE_STRIDE, "stage tail too small");
+    const int zcol = ZS == 1 ? 0 : bz - kb;  // the edge column within the tile
+    const bool zedge = ZE && lane == (zcol & 31);
+    const int zc = ZE ? zcol >> 5 : 0;
+    auto zstage = [&](int q) {  // one cp.async group per call (empty past the last plane)
+        if (!ZE || warp != 0) return;
+        if (q <= nplanes - 2 && jb + lane <= by) {
+            const double *src = Z.zin[ZS == 2] + (size_t)(ib - 2 + q) * by + (jb + lane - 1);
+            const uint32_t dst = hx::smem_addr(smem + (q % NSTAGE) * STAGE_STRIDE + ZG_OFF) + 8 * lane;
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(dst), "l"(src) : "memory");
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    auto zpatch = [&](double *S) {  // the values fetched last into the staged plane
-        if (!zrow) return;
-        if (zlo) S[(1 + lane) * BOX_Z + (0 - kload)] = zg0;
-        if (zhi) S[(1 + lane) * BOX_Z + (bz + 1 - kload)] = zg1;
+    auto zwait = [&]() {  // all groups but the newest have landed
+        if (ZE && warp == 0) asm volatile("cp.async.wait_group 1;" ::: "memory");
     };
-    // ZE: the face cells' copies into the neighbours' slots
-    double *zdst0 = nullptr, *zdst1 = nullptr;
-    unsigned zmask0 = 0, zmask1 = 0;
-    if (ZE && zlo && lane == (1 - kb)) {  // k = 1 is column 0 of the tile: lane 0, first half
-        zdst0 = Z.zout[0] + (size_t)(ib - 1) * by + (jb + row0 - 1);
-        zmask0 = 0x55u;
-    }
-    if (ZE && zhi && lane == ((bz - kb) & 31)) {
-        zdst1 = Z.zout[1] + (size_t)(ib - 1) * by + (jb + row0 - 1);
-        zmask1 = ((bz - kb) >> 5) ? 0xAAu : 0x55u;
-    }
+    // the edge lane's face cells also go to the neighbour's slot (offset of
+    // this thread's first row there; the pointer is formed at the store)
+    unsigned zoff = (unsigned)((ib - 1) * by + (jb + row0 - 1));
+    zstage(1);
+    zstage(2);
 
     double xm[PTS], x0[PTS];
     unsigned long long worst = 0;
@@ -313,12 +317,7 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
         const double *s1 = reinterpret_cast<const double *>(smem + STAGE_STRIDE);
         hx::mbar_wait(&bar[0], 0);
         hx::mbar_wait(&bar[1], 0);
-        if (ZE && (zlo || zhi) && warp == 0) {
-            zfetch(ib);
-            zpatch(reinterpret_cast<double *>(smem + STAGE_STRIDE));  // plane ib: stage 1
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (nplanes - 2 >= 2) zfetch(ib + 1);  // the next relaxed plane, ahead
-        }
+        zwait();  // plane 1's slot rows (the barrier below publishes them)
 #pragma unroll
         for (int p = 0; p < PTS; ++p) {
             const int o = soff + (p >> 1) * BOX_Z + 32 * (p & 1);
@@ -343,21 +342,17 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     for (int q = 1; q <= nplanes - 2; ++q) {
         const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;  // stage holding plane q+1
         hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
-        // plane q + 1's ghost column, for its own relax next iteration (the
-        // barrier below orders it; relax_plane(q) reads only its centres)
-        if (ZE && (zlo || zhi) && warp == 0 && q + 1 <= nplanes - 2) {
-            zpatch(reinterpret_cast<double *>(smem + s_n * STAGE_STRIDE));  // plane q + 1
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-            if (q + 2 <= nplanes - 2) zfetch(ib - 1 + q + 2);
-        }
-        relax_plane<RES, BOX_Z, ZE, true>(
+        relax_plane<RES, BOX_Z, ZS, true>(
             reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
             reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE), soff, BOX_Z, BOX_Z, xm,
-            x0, out, bz, live, worst, zdst0, zmask0, zdst1, zmask1, 1);
+            x0, out, bz, live, worst, zedge, zc,
+            reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE + ZG_OFF) + row0,
+            ZE ? Z.zout[ZS == 2] + zoff : nullptr);
         out += plane;
         if (ZE) {
-            if (zdst0) zdst0 += by;
-            if (zdst1) zdst1 += by;
+            zoff += by;
+            zstage(q + 2);
+            zwait();  // plane q + 1's slot rows, published by the barrier below
         }
         __syncthreads();  // all warps are done with stage s_c (plane q)
         if (threadIdx.x == 0) {
@@ -371,6 +366,27 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
         s_c = s_n;
     }
     if (RES) warp_max_to_global(worst, res);
+}
+
+template <bool RES, int BOX_Z, bool ZE>
+__global__ void __launch_bounds__(THREADS, MIN_CTAS)
+stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__ nxt, int by,
+                   int bz, int i0, int i1, int j0, int j1, int k0, int k1, int klive, int ntj,
+                   int ntk, int chunk, int nchunks, int grows, unsigned long long *res, ZEdge Z) {
+    const Item it = work_item(j0, k0, i0, i1, ntj, ntk, chunk, nchunks, grows);
+    if constexpr (ZE) {  // z-edge tile: holds k = 1 (-z neighbour) / k = bz (+z neighbour)
+        const bool zlo = Z.flag[0] && it.kb <= 1 && 1 < it.kb + TZ && k0 <= 1;
+        const bool zhi = Z.flag[1] && it.kb <= bz && bz < it.kb + TZ && bz < k1;
+        // one instance per side, so a tile keeps one side's state (the host
+        // rejects blocks where one tile would hold both z faces, bz <= TZ)
+        if (zlo && zhi) {
+            if (threadIdx.x == 0 && Z.err) atomicExch(Z.err, HX_E_INVALID);
+            return;
+        }
+        if (zlo) return tma_tile<RES, BOX_Z, 1>(map, nxt, by, bz, j1, k1, klive, it, res, Z);
+        if (zhi) return tma_tile<RES, BOX_Z, 2>(map, nxt, by, bz, j1, k1, klive, it, res, Z);
+    }
+    tma_tile<RES, BOX_Z, 0>(map, nxt, by, bz, j1, k1, klive, it, res, Z);
 }
 
 // ------------------------------------------- row-pair tensor pipeline ----
@@ -1589,6 +1605,7 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
         return HX_E_INVALID;  // whole rows in z: the box holds both z faces
     if (i0 >= i1 || j0 >= j1) return 0;
     if (!tma_eligible(cur, bz)) return HX_E_INVALID;
+    if (zflag[0] && zflag[1] && bz <= TZ) return HX_E_INVALID;  // a tile would hold both faces
     ZEdge Z;
     memset(&Z, 0, sizeof(Z));
     for (int h = 0; h < 2; ++h) {
@@ -1602,17 +1619,22 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
     Z.err = err;
     g_last_variant = 1;
     cudaStream_t st = (cudaStream_t)stream;
-    // Only the tile columns that hold k = 1 (with a -z neighbour) or k = bz
-    // (with a +z neighbour) take the z-edge kernel (more registers, a flag
-    // wait, slot patches); the rest is one plain sweep on the same tile grid,
-    // launched first. A narrow strip sweep runs at about half the HBM rate
-    // (each tile row opens its own DRAM page), so a side without a z
-    // neighbour stays in the main sweep (ncu: profiles/r2_zface_dram.md).
+    // One sweep over whole rows: the tiles that hold k = 1 (with a -z
+    // neighbour) or k = bz (+z) take the z-edge work (flag wait, slot patches,
+    // face copies) at run time; the rest run the plain path. Keeping the edge
+    // tiles in the main sweep's schedule shares their DRAM pages with the
+    // neighbouring tiles: a separate 64-wide strip sweep runs at about half
+    // the HBM rate (profiles/r2_zface_dram.md). HX_ZE_STRIPS=1 restores the
+    // split launches (middle, then edge strips) for comparison.
+    static int strips = -1;
+    if (strips < 0) {
+        const char *e = getenv("HX_ZE_STRIPS");
+        strips = e ? atoi(e) : 0;
+    }
     const int klo_end = 1 + TZ;                       // the first tile column: [1, 1 + TZ)
     const int khi_beg = 1 + ((bz - 1) / TZ) * TZ;     // the tile column holding k = bz
-    if (khi_beg <= klo_end) {  // one or two tile columns: everything is an edge
+    if (!strips || khi_beg <= klo_end)
         return launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, 1, bz + 1, res, st, &Z);
-    }
     const int mid0 = Z.flag[0] ? klo_end : 1, mid1 = Z.flag[1] ? khi_beg : bz + 1;
     if (int rc = launch_tma(cur, nxt, bx, by, bz, i0, i1, j0, j1, mid0, mid1, res, st)) return rc;
     ZEdge lo = Z, hi = Z;

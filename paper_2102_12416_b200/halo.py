@@ -237,13 +237,16 @@ class HaloJacobi:
     """
 
     e2e_ring_slots = 4096  # device residual slots of step_e2e (zeroed when the ring wraps)
-    # fused, z neighbours: True = the interior sweep produces and consumes the
-    # z faces (hx_stencil_box_z: two z-edge strip launches + hx_zsignal);
-    # False = the boundary kernel's z tiles do (default: measured faster, 18.04
-    # vs 19.56 ms for two 1536^3 blocks with a z split on one GPU,
-    # tools/prof_zshell.py — the edge strips run at 2 CTAs/SM and pay a slot
-    # patch per plane, more than the z tiles' scattered sectors cost)
-    z_from_interior = False
+    # fused, z neighbours: True (default) = the interior sweep produces and
+    # consumes the z faces (hx_stencil_box_z: one launch whose edge tiles
+    # wait for the z flags, take the ghost column from the slot and write the
+    # face into the neighbour's slot; hx_zsignal releases the flags). The
+    # sweep opens those DRAM pages anyway, so the z faces cost nothing extra:
+    # 8.92 vs 9.07 ms per step for a 1536^3 block with a z split on 2 GPUs
+    # (plain sweep 8.87). False = the boundary kernel's z tiles, which pay a
+    # DRAM page activation per face cell (tools/prof_zshell.py,
+    # profiles/r2_zface_dram.md).
+    z_from_interior = True
     z_slots = True  # fused exchange: z faces through the contiguous arena slots (False: ghost columns)
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
@@ -466,9 +469,12 @@ class HaloJacobi:
         """Fused exchange with z neighbours: the interior TMA sweep spans
         whole z rows and produces / consumes the z faces itself
         (hx_stencil_box_z), so no kernel touches the z columns separately.
-        Needs a TMA-describable block (even bz, 16-byte aligned field)."""
+        Needs a TMA-describable block (even bz, 16-byte aligned field) and,
+        with both z neighbours, bz > 64 (no tile holds both z faces)."""
+        both = 4 in b.nbr_dirs and 5 in b.nbr_dirs
         return (self.z_from_interior and self.z_slots and (4 in b.nbr_dirs or 5 in b.nbr_dirs)
-                and (b.bz + 2) % 2 == 0 and b.fields[0].data_ptr() % 16 == 0 and b.bz >= 2)
+                and (b.bz + 2) % 2 == 0 and b.fields[0].data_ptr() % 16 == 0 and b.bz >= 2
+                and not (both and b.bz <= 64))
 
     def fused_boxes(self, b: HaloBlock):
         """(interior box, boundary slabs) of a fused step: boxes(), except

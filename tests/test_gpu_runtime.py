@@ -596,10 +596,11 @@ def test_persistent_kernel_timeout_stops_every_cta(pkg):
     eng.close()
 
 
-@pytest.mark.parametrize("dims,pes", [((32, 40, 64), 2), ((48, 48, 48), 8), ((40, 32, 96), 4)])
+@pytest.mark.parametrize("dims,pes", [((32, 40, 64), 2), ((48, 48, 48), 8), ((40, 32, 96), 4),
+                                      ((24, 32, 240), 3)])
 def test_fused_z_faces_from_the_interior_sweep_bitexact(pkg, dims, pes):
     """The alternative z-face path (HaloJacobi.z_from_interior: hx_stencil_box_z
-    edge strips wait for the z flags, patch the ghost column from the slots
+    edge tiles wait for the z flags, patch the ghost column from the slots
     and write the neighbour's slot; hx_zsignal releases the z flags) gives the
     oracle's bits, through eager steps, graph replays and persistent runs."""
     from oracle import jacobi_np
