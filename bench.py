@@ -444,6 +444,10 @@ def main() -> int:
     achieved = ALG_BYTES_PER_CELL * sweep_cells / (sten_ms * 1e-3) / 1e9
     traffic, traffic_ratio = ncu_traffic(ALG_BYTES_PER_CELL * sweep_cells)
     face_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs)
+    # with z faces produced by the interior sweep (HaloJacobi.z_interior), the
+    # boundary kernel (the timed exchange) carries only the x / y faces
+    zint = world > 1 and eng.exchange == "fused" and eng.z_interior(b)
+    shell_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs if not (zint and d >= 4))
 
     # ---- the exchange alone (not sharing HBM with an interior sweep): a few
     # untimed-for-value steps with the overlap split off, for the NVLink fraction
@@ -512,17 +516,21 @@ def main() -> int:
                          "kernel": "stencil_tma_kernel", "peak_kind": peak_kind,
                          "kernel_ms": sten_ms,
                          "alg_bytes_per_launch": ALG_BYTES_PER_CELL * sweep_cells},
-            "halo": ({"bytes_out_per_rank": face_bytes, "exchange_ms": xch_ms,
-                      "exchange_gbs": face_bytes / (xch_ms * 1e-3) / 1e9 if xch_ms else None,
-                      "nvlink_frac": face_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS if xch_ms
+            "halo": ({"bytes_out_per_rank": face_bytes,
+                      "boundary_kernel_bytes": shell_bytes,
+                      "z_faces_in_interior_sweep": bool(zint),
+                      "exchange_ms": xch_ms,
+                      "exchange_gbs": shell_bytes / (xch_ms * 1e-3) / 1e9 if xch_ms else None,
+                      "nvlink_frac": shell_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS if xch_ms
                       else None,
                       "overlap": eng.overlap, "exposed_ms": exposed_ms,
                       "interior_ms": mean_ms("interior"), "shell_ms": mean_ms("shell"),
                       "non_overlapped_frac": exposed_ms / (t_ms / args.steps),
                       "isolated_exchange_ms": iso_ms,
-                      "isolated_exchange_gbs": (face_bytes / (iso_ms * 1e-3) / 1e9) if iso_ms else None,
-                      "isolated_nvlink_frac": (face_bytes / (iso_ms * 1e-3) / 1e9 / NVLINK_GBS)
-                      if iso_ms else None} if world > 1 else None),
+                      "isolated_exchange_gbs": (shell_bytes / (iso_ms * 1e-3) / 1e9)
+                      if iso_ms and shell_bytes else None,
+                      "isolated_nvlink_frac": (shell_bytes / (iso_ms * 1e-3) / 1e9 / NVLINK_GBS)
+                      if iso_ms and shell_bytes else None} if world > 1 else None),
             "gpu_launches": launches,
             "clocks": clk,
             "cpu_baseline": cpu,
