@@ -217,13 +217,13 @@ __device__ __forceinline__ Item work_item(int j0, int k0, int i0, int i1, int nt
 // ------------------------------------------------------- TMA pipeline ----
 // Work item = (tile j, tile k, x chunk). Box in interior coordinates:
 // [i0,i1) x [j0,j1) x [k0,k1).
-// The fused exchange's z faces produced by the interior sweep (round 2):
-// the tiles that hold k = 1 (with a -z neighbour) or k = bz (+z) wait for
-// that neighbour's flag (>= *step + 1), take the ghost column from its slot
-// (packed [i-1][j-1], patched into the staged planes) and copy the face
-// cells into the neighbour's slot. The z ghosts cost no extra HBM traffic:
-// the sweep stages those rows anyway, where a separate z-face kernel reads
-// one 32-byte sector per cell from rows 12 KB apart.
+// The fused exchange's z faces produced by the interior sweep (round 2,
+// the default): the tiles that hold k = 1 (with a -z neighbour) or k = bz
+// (+z) wait for that neighbour's flag (>= *step + 1), take the ghost column
+// from its slot (packed [i-1][j-1], staged beside each plane by cp.async)
+// and copy the face cells into the neighbour's slot. The z faces cost no
+// extra DRAM work: the sweep opens those pages anyway, where a separate
+// z-face kernel pays a page activation per cell (profiles/r2_zface_dram.md).
 struct ZEdge {
     const unsigned long long *flag[2];  // our flags from the -z / +z neighbour (null: none)
     const unsigned long long *step;     // device step counter (hx_zsignal advances it)
