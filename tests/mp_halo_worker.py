@@ -86,7 +86,9 @@ def main():
         res = [max(col) for col in zip(*[p[2] for p in parts])]
         verdict = {"bitwise": field.tobytes() == want.tobytes(),
                    "residuals": mode == "graph" or res == wres,
-                   "grid": list(eng.grid), "world": world}
+                   "grid": list(eng.grid), "world": world,
+                   "z_interior": any(eng.z_interior(b) for b in eng.blocks.values())
+                   if exchange == "fused" else False}
         with open(out, "w") as f:
             json.dump(verdict, f)
     eng.close()

@@ -201,22 +201,28 @@ def test_run_jacobi_large_field_prefaulted_readback_vs_c_oracle(oracle_c, pes):
     assert np.array_equal(r["field"].view(np.uint64), want.view(np.uint64))
 
 
-@pytest.mark.parametrize("mode", ["0", "fused", "graph"])
-def test_ipc_engine_two_processes_one_gpu(cuda, tmp_path, mode):
+@pytest.mark.parametrize("mode,dims", [("0", (40, 24, 32)), ("fused", (40, 24, 32)),
+                                       ("graph", (40, 24, 32)), ("fused", (24, 32, 80)),
+                                       ("graph", (24, 32, 80))])
+def test_ipc_engine_two_processes_one_gpu(cuda, tmp_path, mode, dims):
     """torchrun, 2 ranks, both on cuda:0: arenas and fields exported with
     cudaIpcGetMemHandle, opened by the other process, flags and peer stores
-    across processes; bit-exact vs the numpy oracle (+ residual history)."""
+    across processes; bit-exact vs the numpy oracle (+ residual history).
+    (24, 32, 80) splits z: the z faces go through IPC-mapped slots, produced
+    and consumed by each process's interior sweep."""
     out = tmp_path / "verdict.json"
     env = dict(os.environ, HX_SAME_GPU="1")
+    port = 29633 + ["0", "fused", "graph"].index(mode) + (10 if dims[2] == 80 else 0)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
-           "--master-addr", "127.0.0.1",
-           "--master-port", str(29633 + ["0", "fused", "graph"].index(mode)),
-           os.path.join(ROOT, "tests", "mp_halo_worker.py"), "40", "24", "32", "8", str(out), mode]
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "mp_halo_worker.py"), *map(str, dims), "8", str(out), mode]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     v = json.loads(out.read_text())
     assert v["bitwise"] and v["residuals"], v
     assert v["world"] == 2
+    if dims[2] == 80:
+        assert v["grid"] == [1, 1, 2] and v["z_interior"], v
 
 
 def test_step_e2e_residual_ring_wraps(cuda):
