@@ -346,6 +346,10 @@ def main() -> int:
                          "fused: the boundary sweep stores into the neighbours' ghost planes "
                          "itself (hx_shell_put); nccl: grouped NCCL send/recv comparison "
                          "(implies --overlap 0)")
+    ap.add_argument("--sweep-exchange", type=int, default=0,
+                    help="fused: 1 = every face produced and consumed by the interior sweep "
+                         "(hx_stencil_exchange, no boundary kernel); 0 = x / y faces by the "
+                         "boundary kernel, z faces by the sweep")
     ap.add_argument("--overlap", type=int, default=1,
                     help="1: interior sweep concurrent with the halo exchange (default)")
     args = ap.parse_args()
@@ -380,6 +384,7 @@ def main() -> int:
                      dist=dist if world > 1 else None,
                      overlap=bool(args.overlap) and args.exchange == "p2p",
                      policy=args.policy, exchange=args.exchange if world > 1 else "p2p")
+    eng.xy_from_interior = bool(args.sweep_exchange)
     b = eng.blocks[rank]
     s = eng.stream_of(b)
 
@@ -422,12 +427,16 @@ def main() -> int:
     if (eng.overlap or eng.exchange == "fused") and b.nbr_dirs:
         inner = (eng.fused_boxes(b) if eng.exchange == "fused" else eng.boxes(b))[0]
         sweep_cells = (inner[1] - inner[0]) * (inner[3] - inner[2]) * (inner[5] - inner[4])
+        if eng.exchange == "fused" and eng.sweep_exchange(b):
+            sweep_cells = b.cells  # the sweep relaxes the whole block
         sten_ms = mean_ms("interior")  # the TMA interior launch alone
         exposed_ms = max_over_ranks(mean_ms("exposed"))
-        if eng.exchange == "fused":
-            # interior + boundary kernel; with z neighbours the interior is three
-            # launches (middle + two z-edge strips) and hx_zsignal follows
-            launches_per_step = 2 + (3 if eng.z_interior(b) else 0)
+        if eng.exchange == "fused" and eng.sweep_exchange(b):
+            launches_per_step = 2  # the sweep with every face, then hx_exchange_signal
+        elif eng.exchange == "fused":
+            # interior sweep + boundary kernel; with z neighbours the sweep
+            # carries the z faces and hx_zsignal follows
+            launches_per_step = 2 + (1 if eng.z_interior(b) else 0)
         else:
             launches_per_step = 1 + len(eng.boxes(b)[1]) + 1 + 2 * len(b.nbr_dirs)
     else:
@@ -447,12 +456,14 @@ def main() -> int:
     # with z faces produced by the interior sweep (HaloJacobi.z_interior), the
     # boundary kernel (the timed exchange) carries only the x / y faces
     zint = world > 1 and eng.exchange == "fused" and eng.z_interior(b)
-    shell_bytes = sum(b.face_elems[d] * 8 for d in b.nbr_dirs if not (zint and d >= 4))
+    swx = world > 1 and eng.exchange == "fused" and eng.sweep_exchange(b)
+    shell_bytes = 0 if swx else sum(b.face_elems[d] * 8 for d in b.nbr_dirs
+                                    if not (zint and d >= 4))
 
     # ---- the exchange alone (not sharing HBM with an interior sweep): a few
     # untimed-for-value steps with the overlap split off, for the NVLink fraction
     iso_ms = None
-    if world > 1 and eng.exchange == "fused":
+    if world > 1 and eng.exchange == "fused" and not eng.sweep_exchange(b):
         barrier()
         one = eng.time_shell_alone()
         barrier()
@@ -506,7 +517,8 @@ def main() -> int:
             "data": data_desc[args.data],
             "config": {"workload": workload,
                        "global_dims": list(dims), "grid": list(eng.grid), "policy": args.policy,
-                       "exchange": eng.exchange if world > 1 else "none (single block)",
+                       "exchange": ("fused, every face inside the interior sweep" if swx
+                                    else eng.exchange) if world > 1 else "none (single block)",
                        "block": [b.bx, b.by, b.bz], "parallelism": f"3d-blocks x{world}",
                        "l2": f"inputs > L2 (2 x {(b.bx + 2) * (b.by + 2) * (b.bz + 2) * 8 / 1e9:.1f} GB "
                              "fields per GPU vs 126 MB L2), no flush needed"},
@@ -518,7 +530,8 @@ def main() -> int:
                          "alg_bytes_per_launch": ALG_BYTES_PER_CELL * sweep_cells},
             "halo": ({"bytes_out_per_rank": face_bytes,
                       "boundary_kernel_bytes": shell_bytes,
-                      "z_faces_in_interior_sweep": bool(zint),
+                      "z_faces_in_interior_sweep": bool(zint or swx),
+                      "all_faces_in_interior_sweep": bool(swx),
                       "exchange_ms": xch_ms,
                       "exchange_gbs": shell_bytes / (xch_ms * 1e-3) / 1e9 if xch_ms else None,
                       "nvlink_frac": shell_bytes / (xch_ms * 1e-3) / 1e9 / NVLINK_GBS if xch_ms

@@ -242,6 +242,27 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
 int hx_zsignal(unsigned long long *const flag[2], unsigned long long *step, const int *err,
                void *stream);
 
+/* The fused step as ONE sweep of the whole block (replaces the boundary
+ * kernel hx_shell_put_z and the interior sweep, cl/jacobi3d.py:157-173's
+ * pack / send / recv / unpack / update for every face): tiles that hold a
+ * face wait for that neighbour's flag[d] >= *step + 1; x / y face cells are
+ * also stored into peer_nxt[d] (neighbour d's next field, same padded shape)
+ * at its ghost plane / row, whose own ghost planes / rows the neighbour has
+ * stored into ours; z faces go through the slots as in hx_stencil_box_z.
+ * flag[d] NULL: no neighbour d. Needs a TMA-describable block and no tile
+ * holding both faces of one axis (bz > 64 with both z neighbours, by > 32
+ * with both y neighbours, bx >= 2 with both x neighbours): else
+ * HX_E_INVALID. Follow it with hx_exchange_signal on the same stream. */
+int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
+                        unsigned long long *res, const unsigned long long *const flag[6],
+                        double *const peer_nxt[6], const unsigned long long *step,
+                        const double *const zin[2], double *const zout[2],
+                        unsigned long long timeout_ns, int *err, void *stream);
+/* Release flag[d] = *step + 2 (non-NULL entries, six threads in parallel;
+ * skipped if *err != 0), then *step += 1. hx_zsignal is its z-only form. */
+int hx_exchange_signal(unsigned long long *const flag[6], unsigned long long *step,
+                       const int *err, void *stream);
+
 /* --------------------------------------------------- persistent channel --
  * The Channel API's metadata-free stream (cl/channels.py:33-102; paper
  * §3.2.2) in its pre-registered device form. One direction is a ring of

@@ -231,16 +231,23 @@ struct ZEdge {
     double *zout[2];                    // the neighbours' slots for the next step
     unsigned long long timeout_ns;
     int *err;
+    // x / y faces in the sweep too (hx_stencil_exchange; null: none): our flags
+    // from the -x +x -y +y neighbours, and for each the element distance from
+    // a cell of our next field to the matching ghost cell in its next field
+    const unsigned long long *xyflag[4];
+    long long xydelta[4];
+    int bx;  // block extent in x (the +x face is plane bx)
 };
 
 // One work item (tile x chunk) of the TMA sweep. ZE: the tile holds k = 1
 // with a -z neighbour (zlo) or k = bz with a +z neighbour (zhi) and does the
 // z-edge work as well; the kernel picks the instance per tile, so the plain
 // tiles of a z-edge launch run the plain code (and registers).
-template <bool RES, int BOX_Z, int ZS>  // ZS: bit 0 the tile holds k = 1 (-z), bit 1 k = bz (+z)
+template <bool RES, int BOX_Z, int ZS, bool XY = false>  // ZS: bit 0 the tile holds k = 1 (-z), bit 1 k = bz (+z)
 __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restrict__ nxt, int by,
                                          int bz, int j1, int k1, int klive, const Item &it,
-                                         unsigned long long *res, const ZEdge &Z) {
+                                         unsigned long long *res, const ZEdge &Z,
+                                         unsigned xym = 0) {  // XY: sides -x +x -y +y (bits)
     constexpr bool ZE = ZS != 0, zlo = (ZS & 1) != 0, zhi = (ZS & 2) != 0;
     constexpr unsigned STAGE_BYTES = BOX_Y * BOX_Z * sizeof(double);
     extern __shared__ __align__(128) unsigned char smem[];
@@ -250,10 +257,13 @@ __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restr
     const int kshift = BOX_Z == TZ + 2 ? 0 : (kb - 1) & 1;  // 16-byte aligned TMA rows
     const int kload = kb - 1 - kshift;
 
-    if (ZE && threadIdx.x == 0 && (zlo || zhi)) {
+    if ((ZE || XY) && threadIdx.x == 0) {
         const unsigned long long want = *(volatile const unsigned long long *)Z.step + 1;
         if (zlo) hx::spin_until(Z.flag[0], want, Z.timeout_ns, Z.err);
         if (zhi) hx::spin_until(Z.flag[1], want, Z.timeout_ns, Z.err);
+        if (XY)
+            for (int d = 0; d < 4; ++d)
+                if ((xym >> d) & 1u) hx::spin_until(Z.xyflag[d], want, Z.timeout_ns, Z.err);
     }
     if (threadIdx.x == 0) {
         hx::prefetch_tmap(&map);
@@ -306,6 +316,7 @@ __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restr
     // the edge lane's face cells also go to the neighbour's slot (offset of
     // this thread's first row there; the pointer is formed at the store)
     unsigned zoff = (unsigned)((ib - 1) * by + (jb + row0 - 1));
+
     zstage(1);
     zstage(2);
 
@@ -348,6 +359,35 @@ __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restr
             x0, out, bz, live, worst, zedge, zc,
             reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE + ZG_OFF) + row0,
             ZE ? Z.zout[ZS == 2] + zoff : nullptr);
+        if (XY) {
+            // x / y faces: the face cells just stored also go to the
+            // neighbour's ghost plane / row, a fixed element distance away in
+            // its next field (read back from L1: v[] is dead by now, and
+            // keeping it live would spill the sweep's registers)
+            // (the sides are recomputed here from the parameters rather than
+            // kept in registers across the relax)
+            const int P = ib - 1 + q;
+            const int xd = (Z.xyflag[0] && P == 1) ? 0 : (Z.xyflag[1] && P == Z.bx) ? 1 : -1;
+            unsigned ylo = 0, yhi = 0;  // this thread's cells on row j = 1 / j = by
+#pragma unroll
+            for (int p = 0; p < PTS; ++p) {
+                const int j = jb + row0 + (p >> 1);
+                if (Z.xyflag[2] && j == 1) ylo |= 1u << p;
+                if (Z.xyflag[3] && j == by) yhi |= 1u << p;
+            }
+            if (xd >= 0 || ylo || yhi) {
+                const long long dx = xd >= 0 ? Z.xydelta[xd] : 0;
+#pragma unroll
+                for (int p = 0; p < PTS; ++p) {
+                    if (!((live >> p) & 1u)) continue;
+                    double *const o = out + (size_t)(p >> 1) * (bz + 2) + 32 * (p & 1);
+                    const double v = *o;
+                    if (xd >= 0) o[dx] = v;
+                    if ((ylo >> p) & 1u) o[Z.xydelta[2]] = v;
+                    if ((yhi >> p) & 1u) o[Z.xydelta[3]] = v;
+                }
+            }
+        }
         out += plane;
         if (ZE) {
             zoff += by;
@@ -377,11 +417,21 @@ stencil_tma_kernel(const __grid_constant__ CUtensorMap map, double *__restrict__
     if constexpr (ZE) {  // z-edge tile: holds k = 1 (-z neighbour) / k = bz (+z neighbour)
         const bool zlo = Z.flag[0] && it.kb <= 1 && 1 < it.kb + TZ && k0 <= 1;
         const bool zhi = Z.flag[1] && it.kb <= bz && bz < it.kb + TZ && bz < k1;
+        // x / y faces this tile holds (the box is the whole block then)
+        const unsigned xym = (Z.xyflag[0] && it.ib == 1 ? 1u : 0u) |
+                             (Z.xyflag[1] && it.ib + it.nplanes - 3 == Z.bx ? 2u : 0u) |
+                             (Z.xyflag[2] && it.jb == 1 ? 4u : 0u) |
+                             (Z.xyflag[3] && it.jb <= by && by < it.jb + TY ? 8u : 0u);
         // one instance per side, so a tile keeps one side's state (the host
         // rejects blocks where one tile would hold both z faces, bz <= TZ)
         if (zlo && zhi) {
             if (threadIdx.x == 0 && Z.err) atomicExch(Z.err, HX_E_INVALID);
             return;
+        }
+        if (xym) {
+            if (zlo) return tma_tile<RES, BOX_Z, 1, true>(map, nxt, by, bz, j1, k1, klive, it, res, Z, xym);
+            if (zhi) return tma_tile<RES, BOX_Z, 2, true>(map, nxt, by, bz, j1, k1, klive, it, res, Z, xym);
+            return tma_tile<RES, BOX_Z, 0, true>(map, nxt, by, bz, j1, k1, klive, it, res, Z, xym);
         }
         if (zlo) return tma_tile<RES, BOX_Z, 1>(map, nxt, by, bz, j1, k1, klive, it, res, Z);
         if (zhi) return tma_tile<RES, BOX_Z, 2>(map, nxt, by, bz, j1, k1, klive, it, res, Z);
@@ -1329,7 +1379,8 @@ int launch_tma(const double *cur, double *nxt, int bx, int by, int bz, int i0, i
     ZEdge Z;
     memset(&Z, 0, sizeof(Z));
     if (zedge) Z = *zedge;
-    const bool ze = zedge && (Z.flag[0] || Z.flag[1]);
+    const bool ze = zedge && (Z.flag[0] || Z.flag[1] || Z.xyflag[0] || Z.xyflag[1] ||
+                              Z.xyflag[2] || Z.xyflag[3]);
     // every tile starts at kb = kt + t*TZ (TZ even): one box width per launch. A
     // box whose first column k0 is even (a sweep trimmed by a -z neighbour)
     // uses the 68-wide box shifted to a 16-byte-aligned start; its stores then
@@ -1651,24 +1702,81 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
 // After a fused step's interior and boundary kernels: release the z
 // neighbours' flags (= *step + 2, cumulative over both kernels' slot
 // writes, which precede this launch on the stream) and advance *step.
-__global__ void zsignal_kernel(unsigned long long *f0, unsigned long long *f1,
-                               unsigned long long *step, const int *err) {
-    const unsigned long long v = *(volatile unsigned long long *)step + 2;
-    __threadfence_system();
-    const bool healthy = !err || *(volatile const int *)err == 0;
-    if (healthy) {
-        if (f0) hx::st_release_sys(f0, v);
-        if (f1) hx::st_release_sys(f1, v);
+// The fused step as ONE sweep: every face of the block is produced and
+// consumed by the interior sweep's edge tiles (x / y: the neighbours store
+// straight into our ghost planes / rows and we into theirs; z: through the
+// slots, as hx_stencil_box_z). flag[d]: our flag from neighbour d (null: no
+// neighbour); peer_nxt[d]: neighbour d's next field (x / y only). The box is
+// the whole block. Release with hx_exchange_signal after the launch.
+int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
+                        unsigned long long *res, const unsigned long long *const flag[6],
+                        double *const peer_nxt[6], const unsigned long long *step,
+                        const double *const zin[2], double *const zout[2],
+                        unsigned long long timeout_ns, int *err, void *stream) {
+    if (!cur || !nxt || bx < 1 || by < 1 || bz < 1 || !step || !flag || !peer_nxt)
+        return HX_E_INVALID;
+    if (!tma_eligible(cur, bz)) return HX_E_INVALID;
+    if (flag[4] && flag[5] && bz <= TZ) return HX_E_INVALID;  // a tile would hold both z faces
+    if (flag[2] && flag[3] && by <= TY) return HX_E_INVALID;  // ... both y faces
+    if (flag[0] && flag[1] && bx < 2) return HX_E_INVALID;    // one plane, both x faces
+    ZEdge Z;
+    memset(&Z, 0, sizeof(Z));
+    for (int h = 0; h < 2; ++h) {
+        Z.flag[h] = flag[4 + h];
+        if (flag[4 + h] && (!zin || !zout || !zin[h] || !zout[h])) return HX_E_INVALID;
+        Z.zin[h] = flag[4 + h] ? zin[h] : nullptr;
+        Z.zout[h] = flag[4 + h] ? zout[h] : nullptr;
     }
-    *step = v - 1;
+    const long long sx = (long long)(by + 2) * (bz + 2), sy = bz + 2;
+    const long long span[2] = {sx * bx, sy * by};
+    for (int d = 0; d < 4; ++d) {
+        Z.xyflag[d] = flag[d];
+        if (!flag[d]) continue;
+        if (!peer_nxt[d]) return HX_E_INVALID;
+        const long long shift = (d & 1) ? -span[d >> 1] : span[d >> 1];  // our face -> its ghost
+        Z.xydelta[d] = ((long long)(intptr_t)peer_nxt[d] - (long long)(intptr_t)nxt) /
+                           (long long)sizeof(double) + shift;
+    }
+    Z.bx = bx;
+    Z.step = step;
+    Z.timeout_ns = timeout_ns;
+    Z.err = err;
+    g_last_variant = 1;
+    return launch_tma(cur, nxt, bx, by, bz, 1, bx + 1, 1, by + 1, 1, bz + 1, res,
+                      (cudaStream_t)stream, &Z);
+}
+
+struct Flags6 {
+    unsigned long long *f[6];
+};
+
+// After a step's sweep (and boundary kernel, if any), stream-ordered behind
+// them: threads 0-5 release their flag = *step + 2 in parallel (each
+// st.release.sys is cumulative over the sweep's peer stores, which precede
+// this launch on the stream); then *step += 1.
+__global__ void signal_flags_kernel(Flags6 F, unsigned long long *step, const int *err) {
+    const unsigned long long v = *(volatile unsigned long long *)step + 2;
+    const bool healthy = !err || *(volatile const int *)err == 0;
+    if (threadIdx.x < 6 && F.f[threadIdx.x] && healthy) hx::st_release_sys(F.f[threadIdx.x], v);
+    __syncthreads();  // every thread has read *step
+    if (threadIdx.x == 0) *step = v - 1;
+}
+
+int hx_exchange_signal(unsigned long long *const flag[6], unsigned long long *step, const int *err,
+                       void *stream) {
+    if (!flag || !step) return HX_E_INVALID;
+    Flags6 F;
+    for (int d = 0; d < 6; ++d) F.f[d] = flag[d];
+    signal_flags_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(F, step, err);
+    HX_LAUNCH_CHECK();
+    return 0;
 }
 
 int hx_zsignal(unsigned long long *const flag[2], unsigned long long *step, const int *err,
                void *stream) {
-    if (!flag || !step) return HX_E_INVALID;
-    zsignal_kernel<<<1, 1, 0, (cudaStream_t)stream>>>(flag[0], flag[1], step, err);
-    HX_LAUNCH_CHECK();
-    return 0;
+    if (!flag) return HX_E_INVALID;
+    unsigned long long *f6[6] = {nullptr, nullptr, nullptr, nullptr, flag[0], flag[1]};
+    return hx_exchange_signal(f6, step, err, stream);
 }
 
 int hx_preload_halo_kernels();  // hx_halo.cu
@@ -1682,7 +1790,7 @@ int hx_preload() {
     cudaFuncAttributes a;
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)shell_put_kernel));
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)face_tma_kernel));
-    HX_TRY(cudaFuncGetAttributes(&a, (const void *)zsignal_kernel));
+    HX_TRY(cudaFuncGetAttributes(&a, (const void *)signal_flags_kernel));
     HX_TRY(cudaFuncGetAttributes(&a, (const void *)fill_kernel));
     return hx_preload_halo_kernels();
 }

@@ -247,6 +247,11 @@ class HaloJacobi:
     # DRAM page activation per face cell (tools/prof_zshell.py,
     # profiles/r2_zface_dram.md).
     z_from_interior = True
+    # fused: True = every face (x / y as well as z) is produced and consumed by
+    # the interior sweep's edge tiles (hx_stencil_exchange: one launch per
+    # block and step, no boundary kernel, no comm stream), then
+    # hx_exchange_signal releases the flags.
+    xy_from_interior = False
     z_slots = True  # fused exchange: z faces through the contiguous arena slots (False: ghost columns)
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
@@ -476,6 +481,18 @@ class HaloJacobi:
                 and (b.bz + 2) % 2 == 0 and b.fields[0].data_ptr() % 16 == 0 and b.bz >= 2
                 and not (both and b.bz <= 64))
 
+    def sweep_exchange(self, b: HaloBlock) -> bool:
+        """xy_from_interior applies to this block: the whole fused step is
+        one hx_stencil_exchange sweep (TMA-describable block; no tile holds
+        both faces of one axis: bz > 64 with both z neighbours, by > 32 with
+        both y neighbours, bx >= 2 with both x neighbours)."""
+        n = b.nbr_dirs
+        return (self.xy_from_interior and self.z_slots and bool(n)
+                and (b.bz + 2) % 2 == 0 and b.fields[0].data_ptr() % 16 == 0
+                and not (4 in n and 5 in n and b.bz <= 64)
+                and not (2 in n and 3 in n and b.by <= 32)
+                and not (0 in n and 1 in n and b.bx < 2))
+
     def fused_boxes(self, b: HaloBlock):
         """(interior box, boundary slabs) of a fused step: boxes(), except
         that with z_interior the interior keeps whole z rows and the z slabs
@@ -638,7 +655,7 @@ class HaloJacobi:
                     b.zstep_dev.fill_(it)
             self._zstep_stale = False
         for b in blocks:
-            if not b.nbr_dirs:
+            if not b.nbr_dirs or self.sweep_exchange(b):
                 continue
             _lib.call("hx_set_device", b.device)
             s, c = self.stream_of(b), self.comm[b.device]
@@ -675,7 +692,17 @@ class HaloJacobi:
             rp = rps[b.rank]
             mark.begin("sweep", b, s)
             mark.begin("interior", b, s)
-            if b.nbr_dirs and self.z_interior(b):
+            if self.sweep_exchange(b):  # the whole step: one sweep with every face
+                nxt = b.cur ^ 1
+                zin, zout = self._zslots(b, it)
+                flags = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
+                peers = [b.peer_fields[d][nxt] if d in b.nbr_dirs and d < 4 else None
+                         for d in range(NDIRS)]
+                _lib.call("hx_stencil_exchange", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by,
+                          b.bz, rp, _lib.ptr_array(flags), _lib.ptr_array(peers),
+                          b.zstep_dev.data_ptr(), zin, zout, self.timeout_ns, b.err_ptr,
+                          s.cuda_stream)
+            elif b.nbr_dirs and self.z_interior(b):
                 inner, _ = self.fused_boxes(b)
                 zin, zout = self._zslots(b, it)
                 zflag = (ctypes.c_void_p * 2)(*[b.flag_ptr(d) if d in b.nbr_dirs else None
@@ -697,7 +724,11 @@ class HaloJacobi:
             if b.rank in shell_done:
                 s.wait_event(shell_done[b.rank])
             mark.end("exposed", b, s)
-            if b.nbr_dirs and self.z_interior(b):  # both kernels done: release the z flags
+            if self.sweep_exchange(b):  # the sweep is done: release every flag
+                sig = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+                _lib.call("hx_exchange_signal", _lib.ptr_array(sig), b.zstep_dev.data_ptr(),
+                          b.err_ptr, s.cuda_stream)
+            elif b.nbr_dirs and self.z_interior(b):  # both kernels done: release the z flags
                 zsig = (ctypes.c_void_p * 2)(*[b.put_flag[d] if d in b.nbr_dirs else None
                                               for d in (4, 5)])
                 _lib.call("hx_zsignal", zsig, b.zstep_dev.data_ptr(), b.err_ptr, s.cuda_stream)

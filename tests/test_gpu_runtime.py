@@ -573,6 +573,34 @@ def test_exchange_soak_mixed_schedules_vs_one_block(pkg, dims, pes, policy):
     assert got.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("dims,pes", [((48, 32, 40), 2), ((40, 96, 48), 2), ((64, 64, 64), 8),
+                                      ((96, 96, 96), 27), ((40, 80, 136), 4), ((48, 40, 200), 3)])
+def test_every_face_in_the_interior_sweep_bitexact(pkg, dims, pes):
+    """HaloJacobi.xy_from_interior: the whole fused step is one sweep per
+    block (hx_stencil_exchange: x / y faces stored straight into the
+    neighbours' ghost planes / rows by the edge tiles, z faces through the
+    slots) and hx_exchange_signal. Eager steps with the residual, graph
+    replays and persistent runs alternate; (3,3,3) mixes blocks that qualify
+    with middle blocks that do not (by = 32 with both y neighbours)."""
+    from oracle import jacobi_np
+    from paper_2102_12416_b200.halo import HaloJacobi
+
+    eng = HaloJacobi(dims, pes, device_of=lambda r: 0, exchange="fused", timeout_s=10,
+                     policy="reference")
+    eng.xy_from_interior = True
+    assert any(eng.sweep_exchange(b) for b in eng.blocks.values())
+    eng.run(3, residual=True)
+    eng.run_graph(4)
+    eng.run_persistent(3)
+    eng.run(2)
+    eng.check_errors()
+    want, wres = jacobi_np.sequential(dims, 12)
+    assert eng.assemble().tobytes() == want.tobytes()
+    got = [max(eng.residuals(r)[i] for r in eng.blocks) for i in range(3)]
+    assert got == wres[:3]
+    eng.close()
+
+
 def test_persistent_kernel_timeout_stops_every_cta(pkg):
     """A neighbour that never runs: every CTA's flag wait times out, still
     arrives at the grid barrier, and the launch ends with HX_E_TIMEOUT in the
