@@ -4,13 +4,13 @@ random fields, compared bit for bit with one block on one GPU (no exchange)
 after the same number of iterations. Catches rare ordering races that the
 short parity tests would miss.
 
-    python tools/soak.py [--iters 3000] [--scale 1]
+    python tools/soak.py [--iters 3000] [--scale 1] [--sweep-exchange]
 """
 import argparse, json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 
-def run(dims, pes, device_of, schedule, policy, seed=None, init=None):
+def run(dims, pes, device_of, schedule, policy, seed=None, init=None, sweepx=False):
     """Run ``schedule`` on a fresh engine whose initial interior is random
     (``seed``: per-block N(0,1)) or ``init`` (a global array); returns the
     initial and the final global interior."""
@@ -19,6 +19,7 @@ def run(dims, pes, device_of, schedule, policy, seed=None, init=None):
 
     eng = HaloJacobi(dims, pes, device_of=device_of, exchange="fused", policy=policy,
                      timeout_s=20)
+    eng.xy_from_interior = sweepx
     if init is None:
         eng.fill_random(seed)
         eng.synchronize()
@@ -43,6 +44,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--iters", type=int, default=3000)
     ap.add_argument("--scale", type=int, default=1, help="multiply every extent")
+    ap.add_argument("--sweep-exchange", action="store_true",
+                    help="every face inside the interior sweep (HaloJacobi.xy_from_interior)")
     a = ap.parse_args()
     two = torch.cuda.device_count() >= 2
     dev2 = (lambda r: r % 2) if two else (lambda r: 0)
@@ -58,7 +61,7 @@ def main():
     for name, dims, pes, policy, sched in cases:
         dims = tuple(a.scale * e for e in dims)
         t = time.perf_counter()
-        init, got, grid = run(dims, pes, dev2, sched, policy, seed=11)
+        init, got, grid = run(dims, pes, dev2, sched, policy, seed=11, sweepx=a.sweep_exchange)
         iters = sum(k for _, k in sched)
         _, want, _ = run(dims, 1, lambda r: 0, [("eager", iters)], policy, init=init)
         same = got.tobytes() == want.tobytes()
