@@ -123,6 +123,28 @@ __device__ __forceinline__ void warp_max_to_global(unsigned long long worst,
     }
 }
 
+// The fused exchange's z faces produced by the interior sweep (round 2,
+// the default): the tiles that hold k = 1 (with a -z neighbour) or k = bz
+// (+z) wait for that neighbour's flag (>= *step + 1), take the ghost column
+// from its slot (packed [i-1][j-1], staged beside each plane by cp.async)
+// and copy the face cells into the neighbour's slot. The z faces cost no
+// extra DRAM work: the sweep opens those pages anyway, where a separate
+// z-face kernel pays a page activation per cell (profiles/r2_zface_dram.md).
+struct ZEdge {
+    const unsigned long long *flag[2];  // our flags from the -z / +z neighbour (null: none)
+    const unsigned long long *step;     // device step counter (hx_zsignal advances it)
+    const double *zin[2];               // this step's slots
+    double *zout[2];                    // the neighbours' slots for the next step
+    unsigned long long timeout_ns;
+    int *err;
+    // x / y faces in the sweep too (hx_stencil_exchange; null: none): our flags
+    // from the -x +x -y +y neighbours, and for each the element distance from
+    // a cell of our next field to the matching ghost cell in its next field
+    const unsigned long long *xyflag[4];
+    long long xydelta[4];
+    int bx;  // block extent in x (the +x face is plane bx)
+};
+
 // One x plane of a tile from two staged planes: P0 holds plane q (y/z
 // neighbours), PP plane q+1; xm/x0 carry planes q-1 and q in registers and
 // are advanced. Stores the live cells of plane q and folds their residual.
@@ -137,13 +159,14 @@ __device__ __forceinline__ void warp_max_to_global(unsigned long long worst,
 // the thread already holds in registers (x0: plane q's values): 2 of the 8
 // y loads per row pair stay in shared memory instead of 8 — 28 shared loads
 // per 8 cells instead of 40 (less shared-memory traffic per cell).
-template <bool RES, int ROWSTEP, int ZS = 0, bool CONSEC = false>
+template <bool RES, int ROWSTEP, int ZS = 0, bool CONSEC = false, bool XY = false>
 __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, int soff, int ylo,
                                             int yhi, double (&xm)[PTS], double (&x0)[PTS],
                                             double *out, int bz, unsigned live,
                                             unsigned long long &worst, bool zedge = false,
                                             int zc = 0, const double *zg = nullptr,
-                                            double *zdst = nullptr) {
+                                            double *zdst = nullptr, const ZEdge *Zx = nullptr,
+                                            int P = 0, int jrow = 0, int by = 0) {
     double v[PTS];
     bool fast = true;
     double prev[2] = {0.0, 0.0};  // CONSEC: row t - 1's plane-q values
@@ -185,6 +208,14 @@ __device__ __forceinline__ void relax_plane(const double *P0, const double *PP, 
             out[(size_t)((p >> 1) * RS) * (bz + 2) + 32 * (p & 1)] = v[p];
             if (RES) worst = max(worst, abs_diff_bits(v[p], xm[p]));
             if (ZS && zedge && (p & 1) == zc) zdst[(p >> 1) * RS] = v[p];  // face -> slot
+            if (XY) {  // x / y faces: also into the neighbour's ghost plane / row
+                double *const o = out + (size_t)((p >> 1) * RS) * (bz + 2) + 32 * (p & 1);
+                if (Zx->xyflag[0] && P == 1) o[Zx->xydelta[0]] = v[p];
+                if (Zx->xyflag[1] && P == Zx->bx) o[Zx->xydelta[1]] = v[p];
+                const int j = jrow + (p >> 1);
+                if (Zx->xyflag[2] && j == 1) o[Zx->xydelta[2]] = v[p];
+                if (Zx->xyflag[3] && j == by) o[Zx->xydelta[3]] = v[p];
+            }
         }
     }
 }
@@ -217,27 +248,6 @@ __device__ __forceinline__ Item work_item(int j0, int k0, int i0, int i1, int nt
 // ------------------------------------------------------- TMA pipeline ----
 // Work item = (tile j, tile k, x chunk). Box in interior coordinates:
 // [i0,i1) x [j0,j1) x [k0,k1).
-// The fused exchange's z faces produced by the interior sweep (round 2,
-// the default): the tiles that hold k = 1 (with a -z neighbour) or k = bz
-// (+z) wait for that neighbour's flag (>= *step + 1), take the ghost column
-// from its slot (packed [i-1][j-1], staged beside each plane by cp.async)
-// and copy the face cells into the neighbour's slot. The z faces cost no
-// extra DRAM work: the sweep opens those pages anyway, where a separate
-// z-face kernel pays a page activation per cell (profiles/r2_zface_dram.md).
-struct ZEdge {
-    const unsigned long long *flag[2];  // our flags from the -z / +z neighbour (null: none)
-    const unsigned long long *step;     // device step counter (hx_zsignal advances it)
-    const double *zin[2];               // this step's slots
-    double *zout[2];                    // the neighbours' slots for the next step
-    unsigned long long timeout_ns;
-    int *err;
-    // x / y faces in the sweep too (hx_stencil_exchange; null: none): our flags
-    // from the -x +x -y +y neighbours, and for each the element distance from
-    // a cell of our next field to the matching ghost cell in its next field
-    const unsigned long long *xyflag[4];
-    long long xydelta[4];
-    int bx;  // block extent in x (the +x face is plane bx)
-};
 
 // One work item (tile x chunk) of the TMA sweep. ZE: the tile holds k = 1
 // with a -z neighbour (zlo) or k = bz with a +z neighbour (zhi) and does the
@@ -353,41 +363,12 @@ __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restr
     for (int q = 1; q <= nplanes - 2; ++q) {
         const int s_n = s_c + 1 == NSTAGE ? 0 : s_c + 1;  // stage holding plane q+1
         hx::mbar_wait(&bar[s_n], ((q + 1) / NSTAGE) & 1);
-        relax_plane<RES, BOX_Z, ZS, true>(
+        relax_plane<RES, BOX_Z, ZS, true, XY>(
             reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE),
             reinterpret_cast<const double *>(smem + s_n * STAGE_STRIDE), soff, BOX_Z, BOX_Z, xm,
             x0, out, bz, live, worst, zedge, zc,
             reinterpret_cast<const double *>(smem + s_c * STAGE_STRIDE + ZG_OFF) + row0,
-            ZE ? Z.zout[ZS == 2] + zoff : nullptr);
-        if (XY) {
-            // x / y faces: the face cells just stored also go to the
-            // neighbour's ghost plane / row, a fixed element distance away in
-            // its next field (read back from L1: v[] is dead by now, and
-            // keeping it live would spill the sweep's registers)
-            // (the sides are recomputed here from the parameters rather than
-            // kept in registers across the relax)
-            const int P = ib - 1 + q;
-            const int xd = (Z.xyflag[0] && P == 1) ? 0 : (Z.xyflag[1] && P == Z.bx) ? 1 : -1;
-            unsigned ylo = 0, yhi = 0;  // this thread's cells on row j = 1 / j = by
-#pragma unroll
-            for (int p = 0; p < PTS; ++p) {
-                const int j = jb + row0 + (p >> 1);
-                if (Z.xyflag[2] && j == 1) ylo |= 1u << p;
-                if (Z.xyflag[3] && j == by) yhi |= 1u << p;
-            }
-            if (xd >= 0 || ylo || yhi) {
-                const long long dx = xd >= 0 ? Z.xydelta[xd] : 0;
-#pragma unroll
-                for (int p = 0; p < PTS; ++p) {
-                    if (!((live >> p) & 1u)) continue;
-                    double *const o = out + (size_t)(p >> 1) * (bz + 2) + 32 * (p & 1);
-                    const double v = *o;
-                    if (xd >= 0) o[dx] = v;
-                    if ((ylo >> p) & 1u) o[Z.xydelta[2]] = v;
-                    if ((yhi >> p) & 1u) o[Z.xydelta[3]] = v;
-                }
-            }
-        }
+            ZE ? Z.zout[ZS == 2] + zoff : nullptr, &Z, ib - 1 + q, jb + row0, by);
         out += plane;
         if (ZE) {
             zoff += by;

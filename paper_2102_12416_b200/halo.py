@@ -247,11 +247,14 @@ class HaloJacobi:
     # DRAM page activation per face cell (tools/prof_zshell.py,
     # profiles/r2_zface_dram.md).
     z_from_interior = True
-    # fused: True = every face (x / y as well as z) is produced and consumed by
-    # the interior sweep's edge tiles (hx_stencil_exchange: one launch per
-    # block and step, no boundary kernel, no comm stream), then
-    # hx_exchange_signal releases the flags.
-    xy_from_interior = False
+    # fused: True (default) = every face (x / y as well as z) is produced and
+    # consumed by the interior sweep's edge tiles (hx_stencil_exchange: one
+    # launch per block and step, no boundary kernel, no comm stream), then
+    # hx_exchange_signal releases the flags. Same box, 1536^3 per GPU:
+    # N = 2 8.899 vs 8.907 ms per step, N = 4 8.910 vs 8.927
+    # (profiles/r2_sweep_exchange_ab_*.jsonl). False = x / y faces by the
+    # concurrent boundary kernel (hx_shell_put_z).
+    xy_from_interior = True
     z_slots = True  # fused exchange: z faces through the contiguous arena slots (False: ghost columns)
 
     def __init__(self, dims, pes: int, local_ranks=None, device_of=None, dist=None,
@@ -726,8 +729,12 @@ class HaloJacobi:
             mark.end("exposed", b, s)
             if self.sweep_exchange(b):  # the sweep is done: release every flag
                 sig = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+                # the "exchange" mark: what is left of the exchange outside the
+                # sweep (the flag release); the face traffic overlaps the sweep
+                mark.begin("exchange", b, s)
                 _lib.call("hx_exchange_signal", _lib.ptr_array(sig), b.zstep_dev.data_ptr(),
                           b.err_ptr, s.cuda_stream)
+                mark.end("exchange", b, s)
             elif b.nbr_dirs and self.z_interior(b):  # both kernels done: release the z flags
                 zsig = (ctypes.c_void_p * 2)(*[b.put_flag[d] if d in b.nbr_dirs else None
                                               for d in (4, 5)])
