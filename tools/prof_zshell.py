@@ -26,6 +26,7 @@ def main():
         zs = mode != "ghost_columns"
         eng.z_slots = zs
         eng.z_from_interior = mode == "interior"
+        eng.xy_from_interior = mode == "interior"  # else the sweep would carry the z faces anyway
         eng.reset()
         for _ in range(3):
             eng.step()
