@@ -432,7 +432,7 @@ def main() -> int:
         sten_ms = mean_ms("interior")  # the TMA interior launch alone
         exposed_ms = max_over_ranks(mean_ms("exposed"))
         if eng.exchange == "fused" and eng.sweep_exchange(b):
-            launches_per_step = 2  # the sweep with every face, then hx_exchange_signal
+            launches_per_step = 1  # the sweep with every face; its last edge tile releases
         elif eng.exchange == "fused":
             # interior sweep + boundary kernel; with z neighbours the sweep
             # carries the z faces and hx_zsignal follows

@@ -252,11 +252,15 @@ int hx_zsignal(unsigned long long *const flag[2], unsigned long long *step, cons
  * flag[d] NULL: no neighbour d. Needs a TMA-describable block and no tile
  * holding both faces of one axis (bz > 64 with both z neighbours, by > 32
  * with both y neighbours, bx >= 2 with both x neighbours): else
- * HX_E_INVALID. Follow it with hx_exchange_signal on the same stream. */
+ * HX_E_INVALID. signal / counter non-NULL: the sweep's last edge tile
+ * releases signal[d] = *step + 2 into the neighbours' arenas and advances
+ * *step itself (counter: a zero-initialised uint32, re-armed by the kernel),
+ * so the step is ONE launch; NULL: follow with hx_exchange_signal. */
 int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
                         unsigned long long *res, const unsigned long long *const flag[6],
-                        double *const peer_nxt[6], const unsigned long long *step,
+                        double *const peer_nxt[6], unsigned long long *step,
                         const double *const zin[2], double *const zout[2],
+                        unsigned long long *const signal[6], unsigned *counter,
                         unsigned long long timeout_ns, int *err, void *stream);
 /* Release flag[d] = *step + 2 (non-NULL entries, six threads in parallel;
  * skipped if *err != 0), then *step += 1. hx_zsignal is its z-only form. */

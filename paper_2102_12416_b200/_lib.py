@@ -118,7 +118,8 @@ _SIGS = {
                           ctypes.POINTER(_V), ctypes.POINTER(_V), _U64, _V, _V], _I),
     "hx_zsignal": ([ctypes.POINTER(_V), _V, _V, _V], _I),
     "hx_stencil_exchange": ([_V, _V, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _V,
-                             ctypes.POINTER(_V), ctypes.POINTER(_V), _U64, _V, _V], _I),
+                             ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V), _V,
+                             _U64, _V, _V], _I),
     "hx_exchange_signal": ([ctypes.POINTER(_V), _V, _V, _V], _I),
     "hx_shell_put_z": ([_V, _V, _I, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64,
                         ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V, ctypes.POINTER(_V),

@@ -143,6 +143,14 @@ struct ZEdge {
     const unsigned long long *xyflag[4];
     long long xydelta[4];
     int bx;  // block extent in x (the +x face is plane bx)
+    // in-kernel release (hx_stencil_exchange): the last edge tile to finish
+    // releases sig[d] = *step + 2 into the neighbours' arenas and advances
+    // *step. Only edge tiles read the ghosts the neighbours overwrite next or
+    // store into theirs, so they alone decide when the step is done for the
+    // neighbours. edge_counter: zero-initialised, re-armed by the last tile.
+    unsigned long long *sig[6];
+    unsigned *edge_counter;  // null: release with hx_exchange_signal instead
+    unsigned edge_items;
 };
 
 // One x plane of a tile from two staged planes: P0 holds plane q (y/z
@@ -387,6 +395,26 @@ __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restr
         s_c = s_n;
     }
     if (RES) warp_max_to_global(worst, res);
+    if constexpr (ZE || XY) {
+        if (Z.edge_counter) {  // the last edge tile releases the step to the neighbours
+            __shared__ int last;
+            __syncthreads();  // this tile's local and peer stores are issued
+            if (threadIdx.x == 0) {
+                __threadfence();  // GPU scope per tile; the releases below are cumulative
+                last = atomicAdd(Z.edge_counter, 1u) + 1u == Z.edge_items;
+                if (last) *Z.edge_counter = 0u;  // re-arm (launches on one stream are ordered)
+            }
+            __syncthreads();
+            if (last) {
+                const unsigned long long v = *(volatile const unsigned long long *)Z.step + 2;
+                const bool healthy = !Z.err || *(volatile const int *)Z.err == 0;
+                if (threadIdx.x < 6 && Z.sig[threadIdx.x] && healthy)
+                    hx::st_release_sys(Z.sig[threadIdx.x], v);
+                __syncthreads();  // every releasing thread has read *step
+                if (threadIdx.x == 0) *(volatile unsigned long long *)Z.step = v - 1;
+            }
+        }
+    }
 }
 
 template <bool RES, int BOX_Z, bool ZE>
@@ -1691,11 +1719,13 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
 // the whole block. Release with hx_exchange_signal after the launch.
 int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
                         unsigned long long *res, const unsigned long long *const flag[6],
-                        double *const peer_nxt[6], const unsigned long long *step,
+                        double *const peer_nxt[6], unsigned long long *step,
                         const double *const zin[2], double *const zout[2],
+                        unsigned long long *const signal[6], unsigned *counter,
                         unsigned long long timeout_ns, int *err, void *stream) {
     if (!cur || !nxt || bx < 1 || by < 1 || bz < 1 || !step || !flag || !peer_nxt)
         return HX_E_INVALID;
+    if (counter && !signal) return HX_E_INVALID;
     if (!tma_eligible(cur, bz)) return HX_E_INVALID;
     if (flag[4] && flag[5] && bz <= TZ) return HX_E_INVALID;  // a tile would hold both z faces
     if (flag[2] && flag[3] && by <= TY) return HX_E_INVALID;  // ... both y faces
@@ -1722,6 +1752,25 @@ int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
     Z.step = step;
     Z.timeout_ns = timeout_ns;
     Z.err = err;
+    if (counter) {
+        // the edge tiles, counted by the kernel's own rule (stencil_tma_kernel):
+        // tile columns holding k = 1 / bz, tile rows holding j = 1 / by, chunks
+        // holding i = 1 / bx — for the sides with a neighbour
+        const Schedule sc = make_schedule(1, bx + 1, 1, by + 1, 1, bz + 1);
+        const long long ntk = sc.ntk, ntj = sc.ntj, nch = sc.nchunks;
+        const bool zl = flag[4], zh = flag[5], yl = flag[2], yh = flag[3], xl = flag[0],
+                   xh = flag[1];
+        // tiles that are edge in some axis = all - (tiles edge in no axis)
+        const long long kin = ntk - (zl ? 1 : 0) - (zh && (!zl || ntk > 1) ? 1 : 0);
+        const long long jin = ntj - (yl ? 1 : 0) - (yh && (!yl || ntj > 1) ? 1 : 0);
+        const long long iin = nch - (xl ? 1 : 0) - (xh && (!xl || nch > 1) ? 1 : 0);
+        const long long edge = ntk * ntj * nch - std::max(0LL, kin) * std::max(0LL, jin) *
+                                                     std::max(0LL, iin);
+        if (edge <= 0 || edge > 0xffffffffLL) return HX_E_INVALID;
+        Z.edge_items = (unsigned)edge;
+        Z.edge_counter = counter;
+        for (int d = 0; d < 6; ++d) Z.sig[d] = signal[d];
+    }
     g_last_variant = 1;
     return launch_tma(cur, nxt, bx, by, bz, 1, bx + 1, 1, by + 1, 1, bz + 1, res,
                       (cudaStream_t)stream, &Z);

@@ -701,10 +701,12 @@ class HaloJacobi:
                 flags = [b.flag_ptr(d) if d in b.nbr_dirs else None for d in range(NDIRS)]
                 peers = [b.peer_fields[d][nxt] if d in b.nbr_dirs and d < 4 else None
                          for d in range(NDIRS)]
+                sig = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
+                # the sweep's last edge tile releases the flags (arena counter 2)
                 _lib.call("hx_stencil_exchange", b.field_ptr(), b.field_ptr(nxt), b.bx, b.by,
                           b.bz, rp, _lib.ptr_array(flags), _lib.ptr_array(peers),
-                          b.zstep_dev.data_ptr(), zin, zout, self.timeout_ns, b.err_ptr,
-                          s.cuda_stream)
+                          b.zstep_dev.data_ptr(), zin, zout, _lib.ptr_array(sig),
+                          b.counters_ptr + 8, self.timeout_ns, b.err_ptr, s.cuda_stream)
             elif b.nbr_dirs and self.z_interior(b):
                 inner, _ = self.fused_boxes(b)
                 zin, zout = self._zslots(b, it)
@@ -727,14 +729,8 @@ class HaloJacobi:
             if b.rank in shell_done:
                 s.wait_event(shell_done[b.rank])
             mark.end("exposed", b, s)
-            if self.sweep_exchange(b):  # the sweep is done: release every flag
-                sig = [b.put_flag[d] if d in b.nbr_dirs else None for d in range(NDIRS)]
-                # the "exchange" mark: what is left of the exchange outside the
-                # sweep (the flag release); the face traffic overlaps the sweep
-                mark.begin("exchange", b, s)
-                _lib.call("hx_exchange_signal", _lib.ptr_array(sig), b.zstep_dev.data_ptr(),
-                          b.err_ptr, s.cuda_stream)
-                mark.end("exchange", b, s)
+            if self.sweep_exchange(b):
+                pass  # the sweep released the flags itself (its last edge tile)
             elif b.nbr_dirs and self.z_interior(b):  # both kernels done: release the z flags
                 zsig = (ctypes.c_void_p * 2)(*[b.put_flag[d] if d in b.nbr_dirs else None
                                               for d in (4, 5)])
