@@ -262,6 +262,10 @@ int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
                         const double *const zin[2], double *const zout[2],
                         unsigned long long *const signal[6], unsigned *counter,
                         unsigned long long timeout_ns, int *err, void *stream);
+/* Host only: how many work items of hx_stencil_exchange's sweep hold a face
+ * of the sides in mask (bit d: neighbour d) — the count its last edge tile
+ * waits for. Exposed so it can be checked without a GPU. */
+int hx_exchange_edge_items(int bx, int by, int bz, int mask, unsigned *out);
 /* Release flag[d] = *step + 2 (non-NULL entries, six threads in parallel;
  * skipped if *err != 0), then *step += 1. hx_zsignal is its z-only form. */
 int hx_exchange_signal(unsigned long long *const flag[6], unsigned long long *step,

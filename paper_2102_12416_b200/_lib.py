@@ -34,7 +34,7 @@ EXPORTS = (
     "hx_stencil_set_variant", "hx_stencil_last_variant", "hx_stencil_set_chunk", "hx_div6_check",
     "hx_init_block", "hx_pack", "hx_unpack", "hx_pack_put", "hx_wait_unpack", "hx_shell_put",
     "hx_shell_put_z", "hx_persist_run", "hx_stencil_box_z", "hx_zsignal",
-    "hx_stencil_exchange", "hx_exchange_signal",
+    "hx_stencil_exchange", "hx_exchange_signal", "hx_exchange_edge_items",
     "hx_chan_send", "hx_chan_recv", "hx_chan_trace", "hx_preload",
     "hx_signal",
     "hx_wait_flag", "hx_read_u64", "hx_pingpong", "hx_pingpong_ll",
@@ -121,6 +121,7 @@ _SIGS = {
                              ctypes.POINTER(_V), ctypes.POINTER(_V), ctypes.POINTER(_V), _V,
                              _U64, _V, _V], _I),
     "hx_exchange_signal": ([ctypes.POINTER(_V), _V, _V, _V], _I),
+    "hx_exchange_edge_items": ([_I, _I, _I, _I, ctypes.POINTER(ctypes.c_uint)], _I),
     "hx_shell_put_z": ([_V, _V, _I, _I, _I, _I, _V, ctypes.POINTER(_V), ctypes.POINTER(_V), _U64,
                         ctypes.POINTER(_V), _U64, _V, _U64, _V, _V, _V, ctypes.POINTER(_V),
                         ctypes.POINTER(_V), _V], _I),

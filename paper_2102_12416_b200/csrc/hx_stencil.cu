@@ -1711,6 +1711,29 @@ int hx_stencil_box_z(const double *cur, double *nxt, int bx, int by, int bz, int
 // After a fused step's interior and boundary kernels: release the z
 // neighbours' flags (= *step + 2, cumulative over both kernels' slot
 // writes, which precede this launch on the stream) and advance *step.
+// Work items of the one-sweep fused step that hold a face (host only): the
+// kernel's own rule (stencil_tma_kernel) — tile columns holding k = 1 / bz,
+// tile rows holding j = 1 / by, chunks holding i = 1 / bx, for the sides
+// in mask (bit d: neighbour d) — over the same schedule (make_schedule).
+// The last of them to finish releases the step, so the count must match.
+int hx_exchange_edge_items(int bx, int by, int bz, int mask, unsigned *out) {
+    if (bx < 1 || by < 1 || bz < 1 || !out || (mask & ~63)) return HX_E_INVALID;
+    const Schedule sc = make_schedule(1, bx + 1, 1, by + 1, 1, bz + 1);
+    const long long ntk = sc.ntk, ntj = sc.ntj, nch = sc.nchunks;
+    const bool xl = mask & 1, xh = mask & 2, yl = mask & 4, yh = mask & 8, zl = mask & 16,
+               zh = mask & 32;
+    // edge in some axis = all - edge in no axis (a side's tiles: the first or
+    // the last column / row / chunk; both sides may share one when there is one)
+    const long long kin = ntk - (zl ? 1 : 0) - (zh && (!zl || ntk > 1) ? 1 : 0);
+    const long long jin = ntj - (yl ? 1 : 0) - (yh && (!yl || ntj > 1) ? 1 : 0);
+    const long long iin = nch - (xl ? 1 : 0) - (xh && (!xl || nch > 1) ? 1 : 0);
+    const long long edge =
+        ntk * ntj * nch - std::max(0LL, kin) * std::max(0LL, jin) * std::max(0LL, iin);
+    if (edge < 0 || edge > 0xffffffffLL) return HX_E_INVALID;
+    *out = (unsigned)edge;
+    return 0;
+}
+
 // The fused step as ONE sweep: every face of the block is produced and
 // consumed by the interior sweep's edge tiles (x / y: the neighbours store
 // straight into our ghost planes / rows and we into theirs; z: through the
@@ -1753,21 +1776,10 @@ int hx_stencil_exchange(const double *cur, double *nxt, int bx, int by, int bz,
     Z.timeout_ns = timeout_ns;
     Z.err = err;
     if (counter) {
-        // the edge tiles, counted by the kernel's own rule (stencil_tma_kernel):
-        // tile columns holding k = 1 / bz, tile rows holding j = 1 / by, chunks
-        // holding i = 1 / bx — for the sides with a neighbour
-        const Schedule sc = make_schedule(1, bx + 1, 1, by + 1, 1, bz + 1);
-        const long long ntk = sc.ntk, ntj = sc.ntj, nch = sc.nchunks;
-        const bool zl = flag[4], zh = flag[5], yl = flag[2], yh = flag[3], xl = flag[0],
-                   xh = flag[1];
-        // tiles that are edge in some axis = all - (tiles edge in no axis)
-        const long long kin = ntk - (zl ? 1 : 0) - (zh && (!zl || ntk > 1) ? 1 : 0);
-        const long long jin = ntj - (yl ? 1 : 0) - (yh && (!yl || ntj > 1) ? 1 : 0);
-        const long long iin = nch - (xl ? 1 : 0) - (xh && (!xl || nch > 1) ? 1 : 0);
-        const long long edge = ntk * ntj * nch - std::max(0LL, kin) * std::max(0LL, jin) *
-                                                     std::max(0LL, iin);
-        if (edge <= 0 || edge > 0xffffffffLL) return HX_E_INVALID;
-        Z.edge_items = (unsigned)edge;
+        int mask = 0;
+        for (int d = 0; d < 6; ++d) mask |= flag[d] ? 1 << d : 0;
+        if (int rc = hx_exchange_edge_items(bx, by, bz, mask, &Z.edge_items)) return rc;
+        if (Z.edge_items == 0) return HX_E_INVALID;  // no neighbour: nothing would release
         Z.edge_counter = counter;
         for (int d = 0; d < 6; ++d) Z.sig[d] = signal[d];
     }

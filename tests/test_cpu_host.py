@@ -131,3 +131,39 @@ def test_readback_row_split_and_prefault():
     for f in futs:
         f.result()
     assert out.shape == (6, 5, 4) and out.dtype == np.float64 and not out.any()
+
+
+def test_exchange_edge_item_count_matches_the_kernel_rule():
+    """hx_exchange_edge_items (how many work items of the one-sweep fused
+    step hold a face; its last edge tile releases the step, so a wrong count
+    would hang the neighbours until the flag timeout) against a brute-force
+    enumeration of the kernel's own schedule and classification
+    (stencil_tma_kernel: tiles of TY x TZ, x chunks of 4 planes)."""
+    import itertools
+    import random
+
+    TY, TZ, CHUNK = 32, 64, 4
+
+    def brute(bx, by, bz, mask):
+        chunk = min(CHUNK, bx)
+        n = 0
+        for jb in range(1, by + 1, TY):
+            for kb in range(1, bz + 1, TZ):
+                for ib in range(1, bx + 1, chunk):
+                    last = min(ib + chunk, bx + 1) - 1
+                    zlo = mask & 16 and kb == 1
+                    zhi = mask & 32 and kb <= bz < kb + TZ
+                    xy = ((mask & 1 and ib == 1) or (mask & 2 and last == bx)
+                          or (mask & 4 and jb == 1) or (mask & 8 and jb <= by < jb + TY))
+                    n += bool(zlo or zhi or xy)
+        return n
+
+    rng = random.Random(7)
+    shapes = [(1, 1, 2), (4, 32, 64), (5, 33, 65), (8, 64, 130), (96, 96, 96), (13, 70, 200)]
+    shapes += [(rng.randint(1, 40), rng.randint(1, 100), 2 * rng.randint(1, 120)) for _ in range(30)]
+    got = ctypes.c_uint(0)
+    fn = _lib.raw("hx_exchange_edge_items")
+    for (bx, by, bz), mask in itertools.product(shapes, [1, 2, 3, 4, 8, 12, 16, 32, 48, 63, 21, 42]):
+        assert fn(bx, by, bz, mask, ctypes.byref(got)) == 0
+        assert got.value == brute(bx, by, bz, mask), (bx, by, bz, mask)
+    assert fn(0, 4, 4, 1, ctypes.byref(got)) != 0
