@@ -282,6 +282,10 @@ __device__ __forceinline__ void tma_tile(const CUtensorMap &map, double *__restr
         if (XY)
             for (int d = 0; d < 4; ++d)
                 if ((xym >> d) & 1u) hx::spin_until(Z.xyflag[d], want, Z.timeout_ns, Z.err);
+        // the ghost planes / rows were stored by the peers (generic proxy, made
+        // visible by the acquires): order them before this tile's TMA reads,
+        // as the boundary kernel does
+        asm volatile("fence.proxy.async.global;" ::: "memory");
     }
     if (threadIdx.x == 0) {
         hx::prefetch_tmap(&map);
